@@ -1,0 +1,130 @@
+/*
+ * mvb_cuda.h -- C ABI of the B200-native VByte codec (libmvb_cuda.so).
+ *
+ * Drop-in boundary for the reference's decode path (arxiv 1503.07387,
+ * "Masked VByte"; reference library `mvbyte`, paths relative to
+ * /root/reference/proj).  Each entry point names the reference interface it
+ * replaces.  Semantics (outputs, DecodeStatus, values_written,
+ * bytes_consumed, strict/permissive) are those of the reference's documented
+ * oracle decode_scalar / decode_delta_scalar (core/include/mvb/vbyte.hpp:51-63),
+ * which decode_stream / decode_delta_stream promise to equal on every
+ * canonical stream (core/include/mvb/decode.hpp:42-54).
+ *
+ * Conventions
+ *   - Data errors are status values, never crashes: MVB_OK / MVB_TRUNCATED /
+ *     MVB_MALFORMED mirror mvb::DecodeStatus (vbyte.hpp:43).  API misuse and
+ *     CUDA failures are negative return codes (the reference throws there:
+ *     decode.cpp:55-56, vbyte.cpp:80-81); no exception crosses this ABI.
+ *   - The caller owns every buffer.  Decoders never read past in + in_len and
+ *     never write past out + count.  On a non-OK status,
+ *     out[values_written .. count) is unspecified (the reference's vector path
+ *     may also store past the last value it reports, stream_loop.hpp:28-29).
+ *   - count == 0 is valid with out == NULL (decode_test.cpp:204-206).
+ *   - "_device" entry points take device pointers and run asynchronously on
+ *     `stream`; they allocate nothing.  Their result lands in device memory
+ *     (res_dev, may be NULL) so back-to-back calls need no host sync.
+ *   - Host-pointer entry points (mvb_decode_stream, ...) are synchronous
+ *     drop-ins for the reference functions of the same name: they copy
+ *     in -> device, decode, copy out -> host on an internal stream, using
+ *     device buffers cached per calling thread.
+ *   - Reentrant per (stream, workspace).  No global mutable state except the
+ *     host wrappers' per-thread buffer cache.
+ */
+#ifndef MVB_CUDA_H
+#define MVB_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *mvb_stream_t; /* == cudaStream_t */
+
+/* mvb::DecodeStatus (vbyte.hpp:43) */
+enum {
+    MVB_OK = 0,
+    MVB_TRUNCATED = 1,
+    MVB_MALFORMED = 2
+};
+
+/* API errors (negative) */
+enum {
+    MVB_ERR_INVALID_ARG = -1, /* null pointer with nonzero size, bad mode, ... */
+    MVB_ERR_WORKSPACE = -2,   /* workspace missing or smaller than mvb_workspace_bytes() */
+    MVB_ERR_CUDA = -3,        /* a CUDA runtime call failed */
+    MVB_ERR_DECREASING = -4   /* mvb_encode_deltas: input decreases (vbyte.cpp:80-81) */
+};
+
+/* mvb::DecodeMode (vbyte.hpp:38-41) */
+enum {
+    MVB_STRICT = 0,    /* reject a fifth byte >= 0x10 */
+    MVB_PERMISSIVE = 1 /* take the fifth byte whole, value mod 2^32 */
+};
+
+/* mvb::DecodeResult (vbyte.hpp:45-49); 24 bytes, same layout on host and device. */
+typedef struct {
+    int32_t status;
+    int32_t reserved;
+    uint64_t values_written;
+    uint64_t bytes_consumed;
+} mvb_result;
+
+/* ---------------------------------------------------------------- device API */
+
+/* Bytes of device workspace a decode of in_len input bytes needs.  The
+ * workspace must be zeroed once (mvb_workspace_init or cudaMemset 0) before
+ * its first use; afterwards each decode leaves it ready for the next. */
+size_t mvb_workspace_bytes(size_t in_len);
+int mvb_workspace_init(void *ws, size_t ws_bytes, mvb_stream_t stream);
+
+/* Replaces mvb::decode_stream (decode.hpp:44-45, decode.cpp:73-82) and
+ * mvb::decode_scalar (vbyte.hpp:55-56, vbyte.cpp:47-57).
+ * Decodes exactly `count` integers from in[0..in_len) into out[0..count).
+ * Returns 0 when the launch was queued (the decode status is in *res_dev),
+ * or a negative MVB_ERR_*. */
+int mvb_decode_device(const uint8_t *in, size_t in_len, size_t count, uint32_t *out, int mode,
+                      mvb_result *res_dev, void *ws, size_t ws_bytes, mvb_stream_t stream);
+
+/* Replaces mvb::decode_delta_stream (decode.hpp:51-52, decode.cpp:88-97) and
+ * mvb::decode_delta_scalar (vbyte.hpp:62-63, vbyte.cpp:63-74): decodes
+ * `count` gaps and writes out[i] = prev + gap[0] + ... + gap[i] (mod 2^32). */
+int mvb_decode_delta_device(const uint8_t *in, size_t in_len, size_t count, uint32_t prev,
+                            uint32_t *out, int mode, mvb_result *res_dev, void *ws,
+                            size_t ws_bytes, mvb_stream_t stream);
+
+/* ------------------------------------------------------------ host drop-ins */
+
+/* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream
+ * (and of decode_scalar / decode_delta_scalar, which have identical results).
+ * Return value: the DecodeStatus (>= 0) or a negative MVB_ERR_*; *res (may be
+ * NULL) receives the full DecodeResult. */
+int mvb_decode_stream(const uint8_t *in, size_t in_len, size_t count, uint32_t *out, int mode,
+                      mvb_result *res);
+int mvb_decode_delta_stream(const uint8_t *in, size_t in_len, size_t count, uint32_t prev,
+                            uint32_t *out, int mode, mvb_result *res);
+
+/* ------------------------------------------------------------------ encoder */
+
+/* vbyte.cpp:9-15 */
+size_t mvb_encoded_size(uint32_t x);
+/* vbyte.cpp:17-25: writes 1..5 bytes, returns the count. */
+size_t mvb_encode_one(uint32_t x, uint8_t *out);
+/* vbyte.cpp:33-39 (host): returns bytes written; out needs
+ * mvb_encoded_length(values, n) bytes (<= 5n). */
+size_t mvb_encoded_length(const uint32_t *values, size_t n);
+size_t mvb_encode_sequence(const uint32_t *values, size_t n, uint8_t *out);
+/* vbyte.cpp:41-45 (host): delta_encode + encode_sequence.  Returns 0 and sets
+ * *out_len, or MVB_ERR_DECREASING (and *bad_index) if values decreases. */
+int mvb_encode_deltas(const uint32_t *sorted_values, size_t n, uint8_t *out, size_t *out_len,
+                      size_t *bad_index);
+
+/* Library build/version string. */
+const char *mvb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MVB_CUDA_H */

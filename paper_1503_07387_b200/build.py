@@ -1,0 +1,73 @@
+"""In-tree build of the native libraries (run here on CPU; the .so files travel
+to the GPU box with the repo snapshot).
+
+  libmvb_cuda.so      the decoder: sm_100a kernels + C ABI (nvcc)
+  libmvb_workload.so  host generators / encoder for bench and test inputs (g++)
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print("+", " ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True, cwd=ROOT)
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_cuda(force: bool = False, verbose: bool = True, ptxas_verbose: bool = False) -> str:
+    target = os.path.join(HERE, "libmvb_cuda.so")
+    sources = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    sources.append(os.path.join(ROOT, "include", "mvb_cuda.h"))
+    if force or _stale(target, sources):
+        cmd = [_nvcc(), *NVCC_FLAGS]
+        if ptxas_verbose:
+            cmd += ["-Xptxas", "-v"]
+        cmd += ["-o", target, os.path.join(CSRC, "mvb_cuda.cu")]
+        _run(cmd, verbose)
+    return target
+
+
+def build_workload(force: bool = False, verbose: bool = True) -> str:
+    target = os.path.join(HERE, "libmvb_workload.so")
+    src = os.path.join(CSRC, "workload.cpp")
+    if force or _stale(target, [src]):
+        cxx = os.environ.get("CXX", "g++")
+        _run([cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-o", target, src], verbose)
+    return target
+
+
+def build_all(force: bool = False, verbose: bool = True) -> None:
+    build_cuda(force, verbose)
+    build_workload(force, verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

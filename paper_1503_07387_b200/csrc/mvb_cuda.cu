@@ -1,0 +1,221 @@
+// mvb_cuda.cu -- C ABI (include/mvb_cuda.h) over the sm_100a VByte kernels.
+//
+// Host side of the drop-in boundary.  Mirrors the reference's public decode
+// entry points (/root/reference/proj/core/include/mvb/decode.hpp:42-54 and
+// vbyte.hpp:51-63) and its encoder (vbyte.cpp:9-45).  There is one decode
+// implementation -- the CUDA kernel -- and no CPU fallback: a missing device
+// or a failed launch is reported as MVB_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/mvb_cuda.h"
+#include "decode_kernel.cuh"
+
+namespace {
+
+using mvbk::Params;
+using mvbk::WsHeader;
+
+constexpr size_t kHeaderBytes = sizeof(WsHeader);
+
+size_t tiles_for(size_t mis, size_t scan_len) {
+    return (mis + scan_len + mvbk::kTile - 1) / mvbk::kTile;
+}
+
+// Bytes the decode of `count` integers can touch: every integer (strict or
+// permissive) spans at most 5 bytes, so nothing past 5*count matters.
+size_t scan_length(size_t in_len, size_t count) {
+    if (count > in_len / 5 + 1) return in_len;
+    return std::min(in_len, count * 5);
+}
+
+template <bool Delta, int Mode>
+cudaError_t launch(const Params& p, cudaStream_t s) {
+    mvbk::vbyte_decode_kernel<Delta, Mode><<<p.n_tiles, mvbk::kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
+                  uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
+                  cudaStream_t stream) {
+    if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
+    if (mode != MVB_STRICT && mode != MVB_PERMISSIVE) return MVB_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
+    if (count == 0 || in_len == 0) {
+        // decode_test.cpp:204-206 (empty request) / internal.hpp:23 (no input)
+        if (res_dev) {
+            mvbk::set_result_kernel<<<1, 1, 0, stream>>>(res_dev, count == 0 ? MVB_OK : MVB_TRUNCATED, 0, 0);
+            if (cudaGetLastError() != cudaSuccess) return MVB_ERR_CUDA;
+        }
+        return 0;
+    }
+    const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
+    const size_t scan = scan_length(in_len, count);
+    const size_t tiles = tiles_for(mis, scan);
+    if (ws == nullptr || ws_bytes < kHeaderBytes + tiles * mvbk::kDescWords * 8) return MVB_ERR_WORKSPACE;
+    if (tiles >= (1ull << 31)) return MVB_ERR_INVALID_ARG;
+
+    Params p;
+    p.in = in;
+    p.mis = static_cast<long long>(mis);
+    p.len = static_cast<long long>(scan);
+    p.count = count;
+    p.out = out;
+    p.prev = prev;
+    p.n_tiles = static_cast<unsigned>(tiles);
+    p.hdr = static_cast<WsHeader*>(ws);
+    p.desc = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
+    p.res_dev = res_dev;
+
+    cudaError_t e;
+    if (delta)
+        e = mode == MVB_STRICT ? launch<true, mvbk::MODE_STRICT>(p, stream)
+                               : launch<true, mvbk::MODE_PERMISSIVE>(p, stream);
+    else
+        e = mode == MVB_STRICT ? launch<false, mvbk::MODE_STRICT>(p, stream)
+                               : launch<false, mvbk::MODE_PERMISSIVE>(p, stream);
+    return e == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+// Device buffers behind the synchronous host drop-ins, cached per thread.
+struct HostCtx {
+    cudaStream_t stream = nullptr;
+    uint8_t* d_in = nullptr;
+    size_t in_cap = 0;
+    uint32_t* d_out = nullptr;
+    size_t out_cap = 0;
+    void* d_ws = nullptr;
+    size_t ws_cap = 0;
+    mvb_result* d_res = nullptr;
+    bool ok = false;
+
+    bool init() {
+        if (ok) return true;
+        if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaMalloc(&d_res, sizeof(mvb_result)) != cudaSuccess) return false;
+        ok = true;
+        return true;
+    }
+    template <class T>
+    static bool grow(T*& p, size_t& cap, size_t need, bool zero) {
+        if (need <= cap) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t n = std::max<size_t>(need, 1u << 20);
+        if (cudaMalloc(reinterpret_cast<void**>(&p), n) != cudaSuccess) return false;
+        if (zero && cudaMemset(p, 0, n) != cudaSuccess) return false;
+        cap = n;
+        return true;
+    }
+};
+
+thread_local HostCtx g_ctx;
+
+int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev, uint32_t* out,
+                int mode, mvb_result* res) {
+    if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
+    if (mode != MVB_STRICT && mode != MVB_PERMISSIVE) return MVB_ERR_INVALID_ARG;
+    HostCtx& c = g_ctx;
+    if (!c.init()) return MVB_ERR_CUDA;
+    const size_t scan = scan_length(in_len, count);
+    const size_t wsb = mvb_workspace_bytes(scan);
+    if (!HostCtx::grow(c.d_in, c.in_cap, scan, false) || !HostCtx::grow(c.d_out, c.out_cap, count * 4, false) ||
+        !HostCtx::grow(c.d_ws, c.ws_cap, wsb, true))
+        return MVB_ERR_CUDA;
+    if (scan && cudaMemcpyAsync(c.d_in, in, scan, cudaMemcpyHostToDevice, c.stream) != cudaSuccess)
+        return MVB_ERR_CUDA;
+    const int rc = decode_device(scan ? c.d_in : nullptr, scan, count, delta, prev, count ? c.d_out : nullptr,
+                                 mode, c.d_res, c.d_ws, c.ws_cap, c.stream);
+    if (rc < 0) return rc;
+    mvb_result r;
+    if (cudaMemcpyAsync(&r, c.d_res, sizeof r, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess) return MVB_ERR_CUDA;
+    if (count && cudaMemcpyAsync(out, c.d_out, count * 4, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess)
+        return MVB_ERR_CUDA;
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) return MVB_ERR_CUDA;
+    if (res) *res = r;
+    return r.status;
+}
+
+inline size_t vb_size(uint32_t x) {
+    return x < (1u << 7) ? 1 : x < (1u << 14) ? 2 : x < (1u << 21) ? 3 : x < (1u << 28) ? 4 : 5;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t mvb_workspace_bytes(size_t in_len) {
+    return kHeaderBytes + (tiles_for(15, in_len) + 1) * mvbk::kDescWords * 8;
+}
+
+int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
+    if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
+    return cudaMemsetAsync(ws, 0, ws_bytes, stream) == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+int mvb_decode_device(const uint8_t* in, size_t in_len, size_t count, uint32_t* out, int mode,
+                      mvb_result* res_dev, void* ws, size_t ws_bytes, mvb_stream_t stream) {
+    return decode_device(in, in_len, count, false, 0, out, mode, res_dev, ws, ws_bytes, stream);
+}
+
+int mvb_decode_delta_device(const uint8_t* in, size_t in_len, size_t count, uint32_t prev, uint32_t* out,
+                            int mode, mvb_result* res_dev, void* ws, size_t ws_bytes, mvb_stream_t stream) {
+    return decode_device(in, in_len, count, true, prev, out, mode, res_dev, ws, ws_bytes, stream);
+}
+
+int mvb_decode_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t* out, int mode, mvb_result* res) {
+    return decode_host(in, in_len, count, false, 0, out, mode, res);
+}
+
+int mvb_decode_delta_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t prev, uint32_t* out,
+                            int mode, mvb_result* res) {
+    return decode_host(in, in_len, count, true, prev, out, mode, res);
+}
+
+size_t mvb_encoded_size(uint32_t x) { return vb_size(x); }
+
+size_t mvb_encode_one(uint32_t x, uint8_t* out) {
+    size_t n = 0;
+    while (x >= 0x80) {
+        out[n++] = static_cast<uint8_t>(x | 0x80);
+        x >>= 7;
+    }
+    out[n++] = static_cast<uint8_t>(x);
+    return n;
+}
+
+size_t mvb_encoded_length(const uint32_t* values, size_t n) {
+    size_t total = 0;
+    for (size_t i = 0; i < n; ++i) total += vb_size(values[i]);
+    return total;
+}
+
+size_t mvb_encode_sequence(const uint32_t* values, size_t n, uint8_t* out) {
+    size_t pos = 0;
+    for (size_t i = 0; i < n; ++i) pos += mvb_encode_one(values[i], out + pos);
+    return pos;
+}
+
+int mvb_encode_deltas(const uint32_t* sorted_values, size_t n, uint8_t* out, size_t* out_len, size_t* bad_index) {
+    uint32_t prev = 0;
+    size_t pos = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (sorted_values[i] < prev) {
+            if (bad_index) *bad_index = i;
+            return MVB_ERR_DECREASING;
+        }
+        pos += mvb_encode_one(sorted_values[i] - prev, out + pos);
+        prev = sorted_values[i];
+    }
+    if (out_len) *out_len = pos;
+    return 0;
+}
+
+const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }
+
+}  // extern "C"

@@ -1,0 +1,292 @@
+"""Python mirror of the reference codec interface, backed by the CUDA C ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+``mvbyte`` (paths relative to /root/reference/proj):
+
+====================================  =========================================
+this module                           reference
+====================================  =========================================
+DecodeMode / DecodeStatus             core/include/mvb/vbyte.hpp:38-43
+DecodeResult                          core/include/mvb/vbyte.hpp:45-49
+DecodeOptions                         core/include/mvb/decode.hpp:20-28
+EncodedBuffer                         core/include/mvb/vbyte.hpp:26-30
+encoded_size / encode_one             core/src/vbyte.cpp:9-31
+encode_sequence / encode_deltas       core/src/vbyte.cpp:33-45
+delta_encode / prefix_sum_scalar      core/src/vbyte.cpp:76-99
+decode_stream / decode_scalar         core/src/decode.cpp:73-86, vbyte.cpp:47-61
+decode_delta_stream / _delta_scalar   core/src/decode.cpp:88-102, vbyte.cpp:63-74
+====================================  =========================================
+
+Every decode runs the sm_100a kernel: host arrays (numpy / bytes) go through
+the synchronous host drop-in (H2D copy, decode, D2H copy); torch CUDA tensors
+go through the device entry points on the current stream.  ``decode_scalar``
+and ``decode_stream`` are the same GPU decode because the reference defines
+them to have identical results (decode.hpp:42-43).  ``DecodeOptions.path``
+and ``scalar_handoff`` select CPU backends in the reference; they are accepted
+for signature compatibility and do not change the result (the reference pins
+that invariance, decode_test.cpp:333-362).
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _lib
+
+
+class DecodeMode(enum.IntEnum):
+    strict = 0      # reject integers whose fifth byte is >= 0x10
+    permissive = 1  # take the fifth byte whole; value reduced mod 2^32
+
+
+class DecodeStatus(enum.IntEnum):
+    ok = 0
+    truncated = 1
+    malformed = 2
+
+
+class DecodePath(enum.IntEnum):
+    auto_select = 0
+    portable = 1
+    vector = 2
+
+
+@dataclass
+class DecodeResult:
+    status: DecodeStatus = DecodeStatus.ok
+    values_written: int = 0
+    bytes_consumed: int = 0
+
+
+@dataclass
+class DecodeOptions:
+    path: DecodePath = DecodePath.auto_select
+    mode: DecodeMode = DecodeMode.strict
+    scalar_handoff: int = 16
+
+
+@dataclass
+class EncodedBuffer:
+    bytes: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+    count: int = 0
+    delta_coded: bool = False
+
+
+class MvbError(RuntimeError):
+    """A negative return code of the C ABI (API misuse or CUDA failure)."""
+
+
+_ERRORS = {-1: "invalid argument", -2: "workspace too small", -3: "CUDA error", -4: "input decreases"}
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise MvbError(f"mvb_cuda: {_ERRORS.get(rc, rc)} ({rc})")
+    return rc
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def _u8(a) -> np.ndarray:
+    if isinstance(a, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(a), dtype=np.uint8)
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+
+
+def _ptr(a: np.ndarray) -> Optional[int]:
+    return a.ctypes.data if a.size else None
+
+
+# ------------------------------------------------------------------ encoder
+
+def encoded_size(x: int) -> int:
+    return int(_lib.lib().mvb_encoded_size(int(x) & 0xFFFFFFFF))
+
+
+def encode_one(x: int) -> bytes:
+    buf = (ctypes.c_uint8 * 5)()
+    n = _lib.lib().mvb_encode_one(int(x) & 0xFFFFFFFF, buf)
+    return bytes(buf[:n])
+
+
+def encode_sequence(values) -> EncodedBuffer:
+    v = _u32(values)
+    L = _lib.lib()
+    n = L.mvb_encoded_length(_ptr(v), v.size)
+    out = np.empty(n, np.uint8)
+    L.mvb_encode_sequence(_ptr(v), v.size, _ptr(out))
+    return EncodedBuffer(out, int(v.size), False)
+
+
+def encode_deltas(sorted_values) -> EncodedBuffer:
+    """delta_encode + encode_sequence; raises ValueError (std::invalid_argument
+    in the reference, vbyte.cpp:80-81) if the input decreases."""
+    v = _u32(sorted_values)
+    out = np.empty(5 * v.size, np.uint8)
+    n = ctypes.c_size_t(0)
+    bad = ctypes.c_size_t(0)
+    rc = _lib.lib().mvb_encode_deltas(_ptr(v), v.size, _ptr(out), ctypes.byref(n), ctypes.byref(bad))
+    if rc == -4:
+        raise ValueError(f"delta_encode: input decreases at index {bad.value}")
+    _check(rc)
+    return EncodedBuffer(out[: n.value].copy(), int(v.size), True)
+
+
+def delta_encode(values) -> np.ndarray:
+    v = _u32(values).astype(np.int64)
+    if v.size and np.any(np.diff(v) < 0):
+        i = int(np.argmax(np.diff(v) < 0)) + 1
+        raise ValueError(f"delta_encode: input decreases at index {i}")
+    return np.diff(v, prepend=0).astype(np.uint32)
+
+
+def prefix_sum_scalar(gaps, prev: int = 0) -> np.ndarray:
+    g = _u32(gaps).astype(np.uint64)
+    return ((np.cumsum(g, dtype=np.uint64) + np.uint64(prev)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+# ------------------------------------------------------------------ decode
+
+def _is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _mode_of(options) -> int:
+    if options is None:
+        return int(DecodeMode.strict)
+    if isinstance(options, DecodeOptions):
+        return int(options.mode)
+    return int(DecodeMode(options))
+
+
+class Decoder:
+    """Device-side decoder state: a workspace and a result slot on one GPU.
+
+    ``decode(in, count, out)`` / ``decode_delta(in, count, prev, out)`` take
+    torch CUDA tensors (uint8 input, int32/uint32 output), queue the kernel on
+    the current stream and return immediately; ``result()`` syncs and reads the
+    DecodeResult.  One Decoder must not be used by two streams at once."""
+
+    def __init__(self, device=None, capacity_bytes: int = 1 << 20):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.res = torch.zeros(3, dtype=torch.int64, device=self.device)  # 24-byte mvb_result
+        self.ws = None
+        self.ws_bytes = 0
+        self._ensure(capacity_bytes)
+
+    def _ensure(self, in_len: int):
+        need = int(_lib.lib().mvb_workspace_bytes(int(in_len)))
+        if need > self.ws_bytes:
+            self.ws = self.torch.zeros(need, dtype=self.torch.uint8, device=self.device)
+            self.ws_bytes = need
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def decode(self, inp, count: int, out, mode: int = 0, in_len: Optional[int] = None) -> None:
+        n = inp.numel() if in_len is None else int(in_len)
+        self._ensure(n)
+        _check(_lib.lib().mvb_decode_device(
+            inp.data_ptr() if n else None, n, int(count), out.data_ptr() if count else None, int(mode),
+            self.res.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream()))
+
+    def decode_delta(self, inp, count: int, prev: int, out, mode: int = 0, in_len: Optional[int] = None) -> None:
+        n = inp.numel() if in_len is None else int(in_len)
+        self._ensure(n)
+        _check(_lib.lib().mvb_decode_delta_device(
+            inp.data_ptr() if n else None, n, int(count), int(prev) & 0xFFFFFFFF,
+            out.data_ptr() if count else None, int(mode),
+            self.res.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream()))
+
+    def result(self) -> DecodeResult:
+        r = self.res.cpu().numpy().view(np.uint64)
+        status = int(np.int64(r[0]) & 0xFFFFFFFF)
+        return DecodeResult(DecodeStatus(status), int(r[1]), int(r[2]))
+
+
+_decoders = {}
+
+
+def _decoder_for(t) -> Decoder:
+    key = t.device.index
+    d = _decoders.get(key)
+    if d is None:
+        d = _decoders[key] = Decoder(t.device)
+    return d
+
+
+def _decode(inp, count, prev, out, options, delta: bool):
+    if isinstance(inp, EncodedBuffer):
+        inp = inp.bytes
+    mode = _mode_of(options)
+    count = int(count)
+    if _is_cuda_tensor(inp):
+        if count and (out is None or not _is_cuda_tensor(out) or out.numel() < count):
+            raise MvbError("decode on CUDA tensors needs a CUDA output tensor with >= count elements")
+        d = _decoder_for(inp)
+        if delta:
+            d.decode_delta(inp, count, prev, out, mode)
+        else:
+            d.decode(inp, count, out, mode)
+        return d.result()
+    src = _u8(inp)
+    if count and (out is None or np.asarray(out).size < count):
+        raise MvbError("decode needs an output array with >= count elements")
+    dst = out if count else np.zeros(0, np.uint32)
+    if not (isinstance(dst, np.ndarray) and dst.dtype in (np.uint32, np.int32) and dst.flags.c_contiguous):
+        raise MvbError("output must be a C-contiguous numpy uint32 array")
+    res = _lib.MvbResult()
+    L = _lib.lib()
+    if delta:
+        rc = L.mvb_decode_delta_stream(_ptr(src), src.size, count, int(prev) & 0xFFFFFFFF,
+                                       _ptr(dst), mode, ctypes.byref(res))
+    else:
+        rc = L.mvb_decode_stream(_ptr(src), src.size, count, _ptr(dst), mode, ctypes.byref(res))
+    _check(rc)
+    return DecodeResult(DecodeStatus(res.status), int(res.values_written), int(res.bytes_consumed))
+
+
+def decode_stream(inp, count=None, out=None, options: Union[DecodeOptions, DecodeMode, int, None] = None):
+    """Decodes exactly ``count`` integers of ``inp`` into ``out`` (decode.hpp:44-47).
+
+    ``decode_stream(buf: EncodedBuffer, out, options)`` is the EncodedBuffer
+    overload (decode.hpp:46-47)."""
+    if isinstance(inp, EncodedBuffer) and (count is None or not np.isscalar(count)):
+        inp, count, out, options = inp.bytes, inp.count, count, out
+    return _decode(inp, count, 0, out, options, delta=False)
+
+
+def decode_delta_stream(inp, count=None, prev=0, out=None, options=None):
+    """Decodes ``count`` gaps into absolute values starting from ``prev``
+    (decode.hpp:51-54).  Overload: ``decode_delta_stream(buf, prev, out, options)``."""
+    if isinstance(inp, EncodedBuffer) and not (count is not None and prev is not None and out is not None
+                                                and np.isscalar(count) and np.isscalar(prev)):
+        inp, count, prev, out, options = inp.bytes, inp.count, count, prev, out
+    return _decode(inp, count, prev, out, options, delta=True)
+
+
+def decode_scalar(inp, count=None, out=None, mode: DecodeMode = DecodeMode.strict):
+    """vbyte.hpp:55-58 (same result as decode_stream by definition)."""
+    return decode_stream(inp, count, out, mode)
+
+
+def decode_delta_scalar(inp, count, prev, out, mode: DecodeMode = DecodeMode.strict):
+    """vbyte.hpp:62-63."""
+    return _decode(inp, count, prev, out, mode, delta=True)
+
+
+def version() -> str:
+    return _lib.lib().mvb_version().decode()

@@ -1,0 +1,283 @@
+"""Parity of the sm_100a decoder (through the C ABI) with the oracle and the
+reference's golden vectors.  Integer work: every comparison is bit-exact,
+including DecodeResult's status, values_written and bytes_consumed."""
+import numpy as np
+import pytest
+
+from oracle import Oracle, PERMISSIVE, STRICT
+from paper_1503_07387_b200 import mvb
+from paper_1503_07387_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_decode(data, count, mode=STRICT, delta=False, prev=0):
+    """Host drop-in path: mvb_decode_stream / mvb_decode_delta_stream."""
+    out = np.zeros(max(count, 1), np.uint32)
+    if delta:
+        r = mvb.decode_delta_stream(np.asarray(data, np.uint8), count, prev, out, mvb.DecodeOptions(mode=mode))
+    else:
+        r = mvb.decode_stream(np.asarray(data, np.uint8), count, out, mvb.DecodeOptions(mode=mode))
+    return (int(r.status), r.values_written, r.bytes_consumed), out[:count]
+
+
+def dev_decode(torch, dev, data, count, mode=STRICT, delta=False, prev=0, in_off=0, out_off=0):
+    """Device path at chosen input/output misalignments (bytes / u32 words)."""
+    data = np.asarray(data, np.uint8)
+    src = torch.zeros(data.size + in_off + 16, dtype=torch.uint8, device=dev)
+    src[in_off:in_off + data.size] = torch.from_numpy(data).to(dev)
+    dst = torch.full((count + out_off + 8,), -1, dtype=torch.int32, device=dev)
+    d = mvb._decoder_for(src)
+    inp = src[in_off:in_off + data.size]
+    out = dst[out_off:out_off + count]
+    if delta:
+        d.decode_delta(inp, count, prev, out, mode, in_len=data.size)
+    else:
+        d.decode(inp, count, out, mode, in_len=data.size)
+    r = d.result()
+    full = dst.cpu().numpy().view(np.uint32)
+    # guard words around the output must be untouched (never writes past out+count)
+    assert (full[:out_off] == 0xFFFFFFFF).all()
+    assert (full[out_off + count:] == 0xFFFFFFFF).all()
+    return (int(r.status), r.values_written, r.bytes_consumed), full[out_off:out_off + count]
+
+
+def check_case(c, got):
+    r, out = got
+    n = c["values_written"]
+    assert r == (c["status"], n, c["bytes_consumed"]), c["name"]
+    assert out[:n].tolist() == c["out"], c["name"]
+
+
+def test_kats_host_path(golden):
+    kat, _ = golden
+    for c in kat:
+        data = np.frombuffer(bytes.fromhex(c["bytes"]), np.uint8)
+        check_case(c, gpu_decode(data, c["count"], c["mode"], c["delta"], c["prev"]))
+
+
+def test_kats_device_path_misaligned(golden, cuda):
+    import torch
+
+    kat, _ = golden
+    for i, c in enumerate(kat):
+        data = np.frombuffer(bytes.fromhex(c["bytes"]), np.uint8)
+        for in_off, out_off in ((0, 0), (i % 16, i % 4), (15, 3), (7, 1)):
+            check_case(c, dev_decode(torch, cuda, data, c["count"], c["mode"], c["delta"], c["prev"],
+                                     in_off, out_off))
+
+
+def test_sizes_sweep_equal_oracle(oracle):
+    # decode_test.cpp:198-221 plus tile-boundary sizes
+    for n in (1, 2, 11, 12, 13, 47, 48, 95, 96, 97, 1000, 1365, 1366, 4095, 4096, 4097, 100000, 300001):
+        v = W.mixed_values(n, n)
+        enc = oracle.encode_sequence(v)
+        r, out = gpu_decode(enc, n)
+        assert r == (0, n, enc.size), n
+        assert np.array_equal(out, v), n
+        rd, outd = gpu_decode(enc, n, delta=True, prev=n * 7919)
+        ro, oo = oracle.decode_delta(enc, n, n * 7919)
+        assert rd == ro and np.array_equal(outd, oo), n
+
+
+def test_acceptance_stream_fuzz_1e6(oracle, golden):
+    _, sums = golden
+    s = sums["acceptance_fuzz_1e6_seed424242"]
+    v = W.mixed_values(1000000, 424242)
+    enc = oracle.encode_sequence(v)
+    r, out = gpu_decode(enc, v.size)
+    assert r == (s["status"], s["values_written"], s["bytes_consumed"])
+    assert oracle.fnv_u32(out) == s["out_fnv"]
+
+
+def test_delta_prev_wraparound(oracle, golden):
+    _, sums = golden
+    g = W.mixed_values(20000, 77)
+    enc = oracle.encode_sequence(g)
+    for prev in (0, 1, 0xFFFFFFF0):
+        s = sums[f"delta_mixed77_prev{prev}"]
+        r, out = gpu_decode(enc, g.size, delta=True, prev=prev)
+        assert r == (s["status"], s["values_written"], s["bytes_consumed"])
+        assert oracle.fnv_u32(out) == s["out_fnv"]
+
+
+def test_count_stop_with_many_following(oracle):
+    v = W.mixed_values(300000, 9)
+    enc = oracle.encode_sequence(v)
+    for count in (1, 100, 4097, 123457, 299999):
+        r, out = gpu_decode(enc, count)
+        ro, oo = oracle.decode(enc, count)
+        assert r == ro and np.array_equal(out, oo), count
+        r, out = gpu_decode(enc, count, delta=True, prev=5)
+        ro, oo = oracle.decode_delta(enc, count, 5)
+        assert r == ro and np.array_equal(out, oo), count
+
+
+def _inject(enc, pos, pattern):
+    b = enc.copy()
+    b[pos:pos + len(pattern)] = pattern
+    return b
+
+
+def test_errors_at_random_positions_match_oracle(oracle):
+    """Malformed / truncated / permissive-run cases inside long streams,
+    including across tile (4 KiB) boundaries."""
+    rng = np.random.default_rng(1234)
+    v = W.mixed_values(60000, 4)
+    enc = oracle.encode_sequence(v)
+    patterns = [
+        [0x80, 0x80, 0x80, 0x80, 0x80, 0x01],        # 6-byte integer
+        [0x81, 0x82, 0x83, 0x84, 0x20],              # fifth byte 0x20
+        [0xFF, 0xFF, 0xFF, 0xFF, 0x7F],              # fifth byte 0x7F
+        [0x80] * 13 + [0x05],                        # long run
+        [0x80] * 40,                                 # very long run
+        [0x81, 0x82, 0x83, 0x84, 0x0F],              # canonical-length max fifth byte
+    ]
+    positions = [int(p) for p in rng.integers(0, enc.size - 64, 30)] + [4094, 4095, 4096, 4097, 8190, 12285]
+    for pos in positions:
+        for pat in patterns:
+            data = _inject(enc, pos, pat)
+            count = v.size
+            for mode in (STRICT, PERMISSIVE):
+                ro, oo = oracle.decode(data, count, mode)
+                r, out = gpu_decode(data, count, mode)
+                assert r == ro, (pos, pat, mode)
+                assert np.array_equal(out[: ro[1]], oo[: ro[1]]), (pos, pat, mode)
+                ro, oo = oracle.decode_delta(data, count, 99, mode)
+                r, out = gpu_decode(data, count, mode, delta=True, prev=99)
+                assert r == ro, (pos, pat, mode, "delta")
+                assert np.array_equal(out[: ro[1]], oo[: ro[1]]), (pos, pat, mode, "delta")
+        # truncation at pos
+        data = enc[:pos]
+        ro, oo = oracle.decode(data, v.size)
+        r, out = gpu_decode(data, v.size)
+        assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), ("trunc", pos)
+
+
+def test_all_continuation_permissive_stream(oracle):
+    for n in (4, 5, 9, 10, 4096, 4100, 20000):
+        data = np.full(n, 0x80 | 0x35, np.uint8)
+        data[::7] = 0xFF
+        count = n // 5 + 2
+        for mode in (STRICT, PERMISSIVE):
+            ro, oo = oracle.decode(data, count, mode)
+            r, out = gpu_decode(data, count, mode)
+            assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (n, mode)
+
+
+def test_window_structures_all_masks(oracle):
+    """acceptance.cpp:192-243 replayed as 16-byte streams: every 12-bit
+    continuation mask with random payloads, strict and permissive."""
+    rng = np.random.default_rng(2024)
+    windows = []
+    for m in range(4096):
+        for _ in range(2):
+            w = rng.integers(0, 128, 16, dtype=np.uint8)
+            for i in range(12):
+                if (m >> i) & 1:
+                    w[i] |= 0x80
+            w[12:] = rng.integers(0, 128, 4, dtype=np.uint8)
+            windows.append(w)
+    # concatenating the windows gives one long adversarial stream too
+    big = np.concatenate(windows)
+    for mode in (STRICT, PERMISSIVE):
+        count = big.size
+        ro, oo = oracle.decode(big, count, mode)
+        r, out = gpu_decode(big, count, mode)
+        assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), mode
+    for w in windows[::37]:
+        for mode in (STRICT, PERMISSIVE):
+            ro, oo = oracle.decode(w, 12, mode)
+            r, out = gpu_decode(w, 12, mode)
+            assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]])
+
+
+def test_five_byte_integers_across_tile_boundaries(oracle):
+    rng = np.random.default_rng(5)
+    for lead in range(0, 8):
+        v = np.concatenate([np.full(lead, 3, np.uint32),
+                            rng.integers(1 << 28, 2**32, 3000, dtype=np.uint64).astype(np.uint32)])
+        enc = oracle.encode_sequence(v)
+        r, out = gpu_decode(enc, v.size)
+        assert r == (0, v.size, enc.size) and np.array_equal(out, v)
+
+
+def test_sorted_lists_round_trip():
+    # acceptance.cpp:287-312 structure: lengths in [2^4, 2^16], sorted uniform ids
+    rng = np.random.default_rng(777)
+    for _ in range(60):
+        e = int(rng.integers(4, 16))
+        n = int(rng.integers(1 << e, min((1 << (e + 1)) - 1, 1 << 16) + 1))
+        s = np.sort(rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32))
+        buf = mvb.encode_deltas(s)
+        got = np.zeros(n, np.uint32)
+        r = mvb.decode_delta_stream(buf, 0, got)
+        assert r.status == mvb.DecodeStatus.ok and np.array_equal(got, s)
+
+
+def test_back_to_back_reuse_and_epochs(oracle, cuda):
+    """Many launches on one workspace (epoch-tagged lookback), sizes shrinking
+    and growing, interleaved with failing decodes."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    d = mvb.Decoder(cuda, capacity_bytes=1 << 22)
+    for it in range(40):
+        n = int(rng.integers(1, 200000))
+        v = W.mixed_values(n, it)
+        enc = oracle.encode_sequence(v)
+        if it % 5 == 3:
+            enc = enc[: enc.size // 2]
+        src = torch.from_numpy(enc).to(cuda)
+        out = torch.zeros(n, dtype=torch.int32, device=cuda)
+        d.decode(src, n, out)
+        r = d.result()
+        ro, oo = oracle.decode(enc, n)
+        assert (int(r.status), r.values_written, r.bytes_consumed) == ro
+        assert np.array_equal(out.cpu().numpy().view(np.uint32)[: ro[1]], oo[: ro[1]])
+
+
+def test_empty_and_zero_count():
+    r, _ = gpu_decode(np.zeros(0, np.uint8), 0)
+    assert r == (0, 0, 0)
+    r, _ = gpu_decode(np.zeros(0, np.uint8), 3)
+    assert r == (1, 0, 0)
+    r, _ = gpu_decode(np.array([1, 2, 3], np.uint8), 0)
+    assert r == (0, 0, 0)
+
+
+@pytest.mark.parametrize("name", ["config1", "config2"] + [f"config5_{p}_{k}" for p in W.C5_POINTS
+                                                            for k in ("plain", "delta")])
+def test_full_size_configs_checksums(name, golden, oracle):
+    _, sums = golden
+    s = sums[name]
+    if name == "config1":
+        w = W.config1()
+    elif name == "config2":
+        w = W.config2()
+    else:
+        _, pt, kind = name.split("_")
+        w = W.config5(pt, kind == "delta")
+    assert oracle.fnv_bytes(w.encoded) == s["in_fnv"]
+    r, out = gpu_decode(w.encoded, w.count, delta=s["delta"], prev=s["prev"])
+    assert r == (s["status"], s["values_written"], s["bytes_consumed"])
+    assert oracle.fnv_u32(out) == s["out_fnv"]
+    assert np.array_equal(out, w.expected())
+
+
+def test_config4_full_size_device(golden, oracle, cuda):
+    import torch
+
+    _, sums = golden
+    s = sums["config4"]
+    w = W.config4()
+    assert w.encoded.size == s["in_len"]
+    src = torch.from_numpy(w.encoded).to(cuda)
+    out = torch.empty(w.count, dtype=torch.int32, device=cuda)
+    d = mvb.Decoder(cuda)
+    d.decode_delta(src, w.count, 0, out)
+    r = d.result()
+    assert (int(r.status), r.values_written, r.bytes_consumed) == (s["status"], s["values_written"],
+                                                                  s["bytes_consumed"])
+    got = out.cpu().numpy().view(np.uint32)
+    assert oracle.fnv_u32(got) == s["out_fnv"]
