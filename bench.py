@@ -1,0 +1,377 @@
+"""Benchmark of the B200 VByte decoder (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one decode of one synthetic stream (BASELINE.json configs[1] by
+default: delta decode of 2^24 gaps, 50% 1-byte / 50% 2-byte).  `value` is
+decoded integers per second over all ranks with inputs resident in HBM; `e2e`
+is the same metric through the host-pointer C-ABI drop-in
+(mvb_decode_delta_stream) with pinned host buffers, H2D and D2H inside the
+timed region.  L2 residency is defeated by rotating 4 input/output buffer
+sets whose total (4 x 92 MB for c2) is well above the 126 MB L2.
+
+Multi-GPU (torchrun): configs c1/c2/c5 are independent replicas per rank
+(weak scaling, no data-path collective); timing is CUDA events
+with barrier + synchronize on both sides and the max over ranks.
+
+--impl reference times the reference's own CPU decoder (oracle/_ref, the
+unmodified reference library built from its sources) on this host's cores:
+one stream per thread, as many threads as the host has, each decoding its
+own replica of the same stream (the reference cannot split one stream,
+SPEC.md:360).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded uint32 integers/sec (billions) and achieved HBM GB/s vs peak"
+UNIT = "Gint/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_ncu_traffic(workload):
+    """dram bytes per launch of the decode kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+def make_workload(name):
+    from paper_1503_07387_b200 import workload as W
+
+    if name == "c1":
+        return W.config1()
+    if name == "c2":
+        return W.config2()
+    if name == "c4":
+        return W.config4()
+    if name.startswith("c5"):
+        # c5_<point>[_delta]
+        parts = name.split("_")
+        return W.config5(parts[1], delta=len(parts) > 2 and parts[2] == "delta")
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+           "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.BAD.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_rate(w, seconds, threads, gate=True):
+    """Reference library (oracle/_ref) decode of the workload stream on `threads`
+    host threads, each decoding its own replica; returns (ints/s, reps)."""
+    from oracle import RefLib
+
+    ref = RefLib()
+    enc = np.ascontiguousarray(w.encoded)
+    outs = [np.empty(w.count + 16, np.uint32) for _ in range(threads)]
+    counts = [0] * threads
+    stop_at = [0.0]
+
+    def work(i):
+        n = 0
+        while True:
+            if w.delta:
+                r, _ = ref.decode_delta_stream(enc, w.count, w.prev, out=outs[i])
+            else:
+                r, _ = ref.decode_stream(enc, w.count, out=outs[i])
+            assert r[0] == 0 and r[1] == w.count
+            n += 1
+            if time.perf_counter() >= stop_at[0] and n >= 1:
+                break
+        counts[i] = n
+
+    if gate:  # correctness gate (runner.cpp:147-165): reference output equals ground truth
+        if w.delta:
+            r, o = ref.decode_delta_stream(enc, w.count, w.prev, out=outs[0])
+        else:
+            r, o = ref.decode_stream(enc, w.count, out=outs[0])
+        assert np.array_equal(o, w.expected()), "reference decode disagrees with ground truth"
+    t0 = time.perf_counter()
+    stop_at[0] = t0 + seconds
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    return sum(counts) * w.count / dt, sum(counts)
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    w = make_workload(args.config)
+    threads = os.cpu_count() or 1
+    # each step: every host thread decodes one replica (bounded: ~ a few s total)
+    rates = []
+    cpu_reference_rate(w, 0.0, 1, gate=True)
+    for _ in range(args.warmup):
+        cpu_reference_rate(w, 0.0, threads, gate=False)
+    t_steps = []
+    for _ in range(args.steps):
+        rate, reps = cpu_reference_rate(w, 0.0, threads, gate=False)
+        t_steps.append(reps * w.count / rate)
+        rates.append(rate)
+    value = w.count * threads * args.steps / sum(t_steps) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {"workload": w.name, "n": w.count, "in_bytes": int(w.encoded.size),
+                                        "bytes_per_int": w.bytes_per_int},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"each step: {threads} threads x 1 full decode of the {w.name} stream "
+                                   f"({w.count} ints) with mvb::decode{'_delta' if w.delta else ''}_stream "
+                                   "(SSE masked path)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_07387_b200 import _lib, mvb
+
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    w = make_workload(args.config)
+    count, in_len = w.count, int(w.encoded.size)
+    R = 4  # rotating buffer sets
+    srcs = [torch.from_numpy(w.encoded).to(dev) for _ in range(R)]
+    outs = [torch.empty(count, dtype=torch.int32, device=dev) for _ in range(R)]
+    dec = mvb.Decoder(dev, capacity_bytes=in_len)
+    expected = torch.from_numpy(w.expected().view(np.int32)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        k = i % R
+        if w.delta:
+            dec.decode_delta(srcs[k], count, w.prev, outs[k])
+        else:
+            dec.decode(srcs[k], count, outs[k])
+
+    # correctness gate
+    for k in range(R):
+        step(k)
+    r = dec.result()
+    assert int(r.status) == 0 and r.values_written == count and r.bytes_consumed == in_len, r
+    for k in range(R):
+        assert torch.equal(outs[k], expected), "GPU decode disagrees with ground truth"
+    del expected
+
+    # warm-up, including a >= 1 s sustained pre-roll so clocks settle
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    i = 0
+    while time.perf_counter() - t0 < args.preroll:
+        for _ in range(64):
+            step(i)
+            i += 1
+        torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for s in range(args.steps):
+            ev[s][0].record(stream)
+            step(s)
+            ev[s][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(stop)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    r = dec.result()
+    assert int(r.status) == 0 and r.values_written == count
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * count * args.steps / (total_ms / 1e3) / 1e9
+
+    # roofline of the decode kernel: algorithmic bytes = input + 4 B per int
+    alg_bytes = in_len + 4 * count
+    avg_kernel_s = statistics.mean(kern_ms) / 1e3
+    achieved = alg_bytes / avg_kernel_s / 1e9
+    peak, peak_kind = load_peaks()
+    traffic = load_ncu_traffic(w.name)
+
+    # end to end through the host C-ABI drop-in with pinned host buffers
+    h_in = torch.from_numpy(w.encoded).pin_memory()
+    h_out = torch.empty(count, dtype=torch.int32).pin_memory()
+    L = _lib.lib()
+    res = _lib.MvbResult()
+
+    def e2e_call():
+        if w.delta:
+            rc = L.mvb_decode_delta_stream(h_in.data_ptr(), in_len, count, w.prev, h_out.data_ptr(), 0,
+                                           ctypes.byref(res))
+        else:
+            rc = L.mvb_decode_stream(h_in.data_ptr(), in_len, count, h_out.data_ptr(), 0, ctypes.byref(res))
+        assert rc == 0 and res.values_written == count, (rc, res.values_written)
+
+    for _ in range(3):
+        e2e_call()
+    assert np.array_equal(h_out.numpy().view(np.uint32), w.expected()), "e2e output mismatch"
+    if world > 1:
+        dist.barrier()
+    e_steps = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        e2e_call()
+    e_dt = time.perf_counter() - t0
+    et = torch.tensor([e_dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = world * count * e_steps / float(et.item()) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        try:
+            rate, reps = cpu_reference_rate(w, args.cpu_seconds, 1)
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"{reps} full decodes of the {w.name} stream ({count} ints) by the reference "
+                             f"library's decode{'_delta' if w.delta else ''}_stream (SSE masked path), 1 thread, "
+                             f"~{args.cpu_seconds:.0f} s"}
+        except Exception as e:  # reference build missing on this host
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": w.name, "n": count, "in_bytes": in_len,
+                       "bytes_per_int": round(w.bytes_per_int, 4), "delta": w.delta,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "l2": f"rotating {R} input/output sets ({R * (in_len + 4 * count) / 1e6:.0f} MB > 126 MB L2)"},
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": statistics.mean(kern_ms),
+                         "kernel_ms_min": min(kern_ms)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_len,
+                    "d2h_bytes_per_step": 4 * count + ctypes.sizeof(_lib.MvbResult),
+                    "api": "mvb_decode_delta_stream (host pointers, pinned)" if w.delta else
+                           "mvb_decode_stream (host pointers, pinned)"},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--preroll", type=float, default=1.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

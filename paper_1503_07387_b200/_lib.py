@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmvb_cuda.so")
+LIB_PATH = os.environ.get("MVB_CUDA_LIB") or os.path.join(HERE, "libmvb_cuda.so")  # override: experiments only
 WORKLOAD_LIB_PATH = os.path.join(HERE, "libmvb_workload.so")
 
 # Every symbol include/mvb_cuda.h declares (checked by tests/test_abi.py).

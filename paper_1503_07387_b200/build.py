@@ -47,6 +47,8 @@ def build_cuda(force: bool = False, verbose: bool = True, ptxas_verbose: bool = 
     sources = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
     sources.append(os.path.join(ROOT, "include", "mvb_cuda.h"))
     if force or _stale(target, sources):
+        if os.path.exists(target):
+            os.remove(target)  # never leave a stale library behind a failed build
         cmd = [_nvcc(), *NVCC_FLAGS]
         if ptxas_verbose:
             cmd += ["-Xptxas", "-v"]

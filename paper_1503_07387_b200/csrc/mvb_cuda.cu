@@ -14,6 +14,7 @@
 
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
+#include "decode_pipelined.cuh"
 
 namespace {
 
@@ -26,6 +27,13 @@ size_t tiles_for(size_t mis, size_t scan_len) {
     return (mis + scan_len + mvbk::kTile - 1) / mvbk::kTile;
 }
 
+size_t groups_for(size_t tiles) { return (tiles + mvbk::kGroup - 1) / mvbk::kGroup; }
+
+// Workspace bytes for a launch of `tiles` tiles (layout in decode_kernel.cuh).
+size_t ws_need(size_t tiles) {
+    return kHeaderBytes + (tiles * mvbk::kDescArrays + groups_for(tiles) * mvbk::kGroupArrays) * 8;
+}
+
 // Bytes the decode of `count` integers can touch: every integer (strict or
 // permissive) spans at most 5 bytes, so nothing past 5*count matters.
 size_t scan_length(size_t in_len, size_t count) {
@@ -33,15 +41,50 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
+int g_kernel_choice = 0;  // 0: pipelined for strict mode (default); 1: per-tile kernel (profiling only)
+
 template <bool Delta, int Mode>
 cudaError_t launch(const Params& p, cudaStream_t s) {
     mvbk::vbyte_decode_kernel<Delta, Mode><<<p.n_tiles, mvbk::kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
+// Persistent launch: as many CTAs as can be co-resident (the lookback of a
+// tile may wait on any earlier tile, so every CTA must be running), capped by
+// the number of tiles.
+template <bool Delta, bool Trace>
+cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
+    static int per_sm = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 0) {
+        e = cudaFuncSetAttribute(mvbk::vbyte_decode_pipelined<Delta, Trace>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mvbk::kSmemBytes);
+        if (e != cudaSuccess) return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_pipelined<Delta, Trace>,
+                                                          mvbk::kPThreads, mvbk::kSmemBytes);
+        if (e != cudaSuccess) return e;
+        per_sm = n > 0 ? n : 1;
+    }
+    const long long cap = static_cast<long long>(per_sm) * sms;
+    const unsigned grid = static_cast<unsigned>(p.n_tiles < cap ? p.n_tiles : cap);
+    mvbk::vbyte_decode_pipelined<Delta, Trace><<<grid, mvbk::kPThreads, mvbk::kSmemBytes, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <bool Delta>
+cudaError_t launch_pipelined(const Params& p, cudaStream_t s) {
+    return p.trace ? launch_pipelined_t<Delta, true>(p, s) : launch_pipelined_t<Delta, false>(p, s);
+}
+
 int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
                   uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, unsigned long long* trace = nullptr) {
     if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
     if (mode != MVB_STRICT && mode != MVB_PERMISSIVE) return MVB_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
@@ -56,7 +99,7 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
     const size_t scan = scan_length(in_len, count);
     const size_t tiles = tiles_for(mis, scan);
-    if (ws == nullptr || ws_bytes < kHeaderBytes + tiles * mvbk::kDescWords * 8) return MVB_ERR_WORKSPACE;
+    if (ws == nullptr || ws_bytes < ws_need(tiles)) return MVB_ERR_WORKSPACE;
     if (tiles >= (1ull << 31)) return MVB_ERR_INVALID_ARG;
 
     Params p;
@@ -68,11 +111,21 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.prev = prev;
     p.n_tiles = static_cast<unsigned>(tiles);
     p.hdr = static_cast<WsHeader*>(ws);
-    p.desc = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
+    p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
+    p.dsum = p.dcnt + tiles;
+    p.dmax = p.dsum + tiles;
+    p.n_groups = static_cast<unsigned>(groups_for(tiles));
+    p.gcnt = p.dmax + tiles;
+    p.gsum = p.gcnt + p.n_groups;
+    p.gacc_cnt = p.gsum + p.n_groups;
+    p.gacc_sum = p.gacc_cnt + p.n_groups;
     p.res_dev = res_dev;
+    p.trace = trace;
 
     cudaError_t e;
-    if (delta)
+    if (mode == MVB_STRICT && g_kernel_choice == 0)
+        e = delta ? launch_pipelined<true>(p, stream) : launch_pipelined<false>(p, stream);
+    else if (delta)
         e = mode == MVB_STRICT ? launch<true, mvbk::MODE_STRICT>(p, stream)
                                : launch<true, mvbk::MODE_PERMISSIVE>(p, stream);
     else
@@ -150,7 +203,7 @@ inline size_t vb_size(uint32_t x) {
 extern "C" {
 
 size_t mvb_workspace_bytes(size_t in_len) {
-    return kHeaderBytes + (tiles_for(15, in_len) + 1) * mvbk::kDescWords * 8;
+    return ws_need(tiles_for(15, in_len) + 1);
 }
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
@@ -215,6 +268,18 @@ int mvb_encode_deltas(const uint32_t* sorted_values, size_t n, uint8_t* out, siz
     if (out_len) *out_len = pos;
     return 0;
 }
+
+// Internal profiling entry (not part of include/mvb_cuda.h): a decode that
+// also records a per-tile timeline (8 x u64 per tile, %globaltimer ns).
+int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta, uint32_t prev, uint32_t* out,
+                       int mode, mvb_result* res_dev, void* ws, size_t ws_bytes, mvb_stream_t stream,
+                       unsigned long long* trace) {
+    return decode_device(in, in_len, count, delta != 0, prev, out, mode, res_dev, ws, ws_bytes, stream, trace);
+}
+
+// Internal profiling switch (not part of include/mvb_cuda.h): 0 = pipelined
+// strict-mode kernel (default), 1 = per-tile kernel for every mode.
+void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
 const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }
 
