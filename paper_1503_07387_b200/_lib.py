@@ -89,6 +89,15 @@ def lib():
     return _lib
 
 
+def set_kernel_choice(choice: int) -> None:
+    """Profiling/testing switch (internal symbol mvbx_set_kernel): strict-mode
+    kernel 0 = CTA-pipelined (default), 1 = per-tile, 2 = warp-tile."""
+    f = lib().mvbx_set_kernel
+    f.argtypes = [ctypes.c_int]
+    f.restype = None
+    f(int(choice))
+
+
 def workload_lib():
     """Host-side generators/encoder used to build bench and test inputs."""
     global _wlib

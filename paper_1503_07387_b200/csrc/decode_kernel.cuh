@@ -169,24 +169,20 @@ __host__ __device__ __forceinline__ uint32_t bmsk(uint32_t width) {
 #endif
 }
 
-// bit i = bit 7 of byte i (a 4-lane movemask).
+// bit i = bit 7 of byte i (a 4-lane movemask): one multiply gathers the four
+// high bits at bits 28..31 (the other partial products land at bits 7, 14,
+// 15, 21, 22, 23 and cannot carry into them).
 __host__ __device__ __forceinline__ uint32_t hibits4(uint32_t x) {
-    return (((x >> 7) & 0x01010101u) * 0x10204080u) >> 28;
+    return ((x & 0x80808080u) * 0x204081u) >> 28;
 }
 
 // 16-bit movemask of four words (bit 4k+r = bit 7 of byte r of word k).
+// Bits 24..27 of each product are zero, so the shifted products need at most
+// a mask to drop the stray partial products.
 __host__ __device__ __forceinline__ uint32_t hibits16(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
-    // Gather word k's high bits at bit k of each byte, then transpose the
-    // 4x4 bit matrix with two delta swaps.
-    uint32_t m = ((w0 >> 7) & 0x01010101u) | ((w1 >> 6) & 0x02020202u) |
-                 ((w2 >> 5) & 0x04040404u) | ((w3 >> 4) & 0x08080808u);
-    m = (m | (m >> 4)) & 0x00FF00FFu;  // byte r, bit k -> bit 4r + k
-    m = (m | (m >> 8)) & 0x0000FFFFu;
-    uint32_t t = (m ^ (m >> 3)) & 0x0A0Au;
-    m ^= t ^ (t << 3);
-    t = (m ^ (m >> 6)) & 0x00CCu;
-    m ^= t ^ (t << 6);
-    return m;
+    const uint32_t p0 = (w0 & 0x80808080u) * 0x204081u, p1 = (w1 & 0x80808080u) * 0x204081u;
+    const uint32_t p2 = (w2 & 0x80808080u) * 0x204081u, p3 = (w3 & 0x80808080u) * 0x204081u;
+    return (p0 >> 28) | (p1 >> 24) | ((p2 >> 20) & 0xF00u) | ((p3 >> 16) & 0xF000u);
 }
 
 // 7-bit digits of the four bytes of w, concatenated little-endian (28 bits).

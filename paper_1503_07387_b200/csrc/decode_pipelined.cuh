@@ -40,7 +40,6 @@ constexpr int kInBuf = kTile + 2 * kHalo;          // tile + 16-byte halos
 constexpr int kVal = kPasses * kPWorkerThreads * 8;  // 4096 values per tile slot
 constexpr int kLag = 2;                            // iterations between decode and lookback
 constexpr unsigned kWorkerBar = 1;                 // named barrier id for the 256 workers
-constexpr unsigned kTileDoneBar = 2;               // workers arrive when a tile's aggregates are out
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -75,15 +74,6 @@ __device__ __forceinline__ void workers_sync() {
     asm volatile("bar.sync %0, %1;" ::"r"(kWorkerBar), "r"(kPWorkerThreads) : "memory");
 }
 
-// Workers signal (without waiting) that tile t_i's aggregates are published;
-// the lookback warp waits for that signal one iteration later, so each
-// arrival is consumed before the next one can happen.
-__device__ __forceinline__ void tile_done_arrive() {
-    asm volatile("bar.arrive %0, %1;" ::"r"(kTileDoneBar), "r"(kPThreads) : "memory");
-}
-__device__ __forceinline__ void tile_done_wait() {
-    asm volatile("bar.sync %0, %1;" ::"r"(kTileDoneBar), "r"(kPThreads) : "memory");
-}
 
 // Tile geometry helpers.
 __device__ __forceinline__ long long tile_pos0(const Params& P, long long t) { return t * kTile - P.mis; }
@@ -281,7 +271,8 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
                 mbar_expect_tx(&bar[cb ^ 1], kInBuf);
                 tma_load_1d(IN[cb ^ 1], P.in + tile_pos0(P, t + G) - kHalo, kInBuf, &bar[cb ^ 1]);
             }
-            if (i >= 1 && i - 1 < my_tiles) tile_done_wait();  // t_{i-1}'s aggregates are out
+            // t_{i-2} was finished by the workers before barrier #1 of iteration
+            // i-1, which this warp has passed: its slots and aggregates are out.
             if (i >= kLag) {
                 const long long tp = t - kLag * G;
                 const int ps = (i - kLag) & 3;
@@ -367,33 +358,40 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
         __syncthreads();  // bar #1: t_i counts; t_{i-2} resolved by the lookback warp
         if (warp == kPLBWarp) continue;
 
-        // ---- workers: store t_{i-2} ----
+        // ---- workers: store t_{i-2}: one thread per 16-byte-aligned output quad ----
         if (i >= kLag) {
             const int ps = (i - kLag) & 3;
-            const unsigned ntp = ntile_lag1;
             const unsigned long long cnt_prefix = s_cnt_pre[ps];
             const uint32_t carry = kDelta ? s_sum_pre[ps] : 0u;
             const unsigned long long room = P.count > cnt_prefix ? P.count - cnt_prefix : 0ull;
-            const unsigned lim = room < ntp ? static_cast<unsigned>(room) : ntp;
-            const unsigned ah =
-                (4u - static_cast<unsigned>(((reinterpret_cast<uintptr_t>(P.out) >> 2) + cnt_prefix) & 3u)) & 3u;
+            const unsigned lim = room < ntile_lag1 ? static_cast<unsigned>(room) : ntile_lag1;
+            // quad q covers tile-local ints 4q-a .. 4q-a+3 at a 16-byte-aligned address
+            const unsigned a = static_cast<unsigned>(((reinterpret_cast<uintptr_t>(P.out) >> 2) + cnt_prefix) & 3u);
+            uint32_t* const qbase = P.out + cnt_prefix - a;
             const uint32_t* vals = VAL[cb];  // (i - 2) & 1 == i & 1
+            const unsigned nq = lim ? (lim + a + 3) >> 2 : 0u;
+            for (unsigned q = tid; q < nq; q += kPWorkerThreads) {
+                const int i0 = static_cast<int>(4 * q) - static_cast<int>(a);
+                if (i0 >= 0 && static_cast<unsigned>(i0) + 4 <= lim) {
+                    uint32_t v0, v1, v2, v3;
+                    if (a == 0) {
+                        const uint4 x = *reinterpret_cast<const uint4*>(vals + i0);
+                        v0 = x.x; v1 = x.y; v2 = x.z; v3 = x.w;
+                    } else if (a == 2) {
+                        const uint2 x = *reinterpret_cast<const uint2*>(vals + i0);
+                        const uint2 y = *reinterpret_cast<const uint2*>(vals + i0 + 2);
+                        v0 = x.x; v1 = x.y; v2 = y.x; v3 = y.y;
+                    } else {  // i0 odd: i0+1 is 8-byte aligned
+                        const uint2 x = *reinterpret_cast<const uint2*>(vals + i0 + 1);
+                        v0 = vals[i0]; v1 = x.x; v2 = x.y; v3 = vals[i0 + 3];
+                    }
+                    stg_stream16(qbase + 4 * q, v0 + carry, v1 + carry, v2 + carry, v3 + carry);
+                } else {
 #pragma unroll
-            for (int p = 0; p < kPasses; ++p) {
-                const unsigned i0 = kPWorkerThreads * 8 * p + 256 * warp;
-                if (i0 >= lim) continue;  // warp-uniform
-                const unsigned u = tid + kPWorkerThreads * p;
-                const uint4 qa = *reinterpret_cast<const uint4*>(vals + 8 * u);
-                const uint4 qb = *reinterpret_cast<const uint4*>(vals + 8 * u + 4);
-                const uint32_t v[8] = {qa.x + carry, qa.y + carry, qa.z + carry, qa.w + carry,
-                                       qb.x + carry, qb.y + carry, qb.z + carry, qb.w + carry};
-                uint32_t* const out_pass = P.out + cnt_prefix + i0;
-                const unsigned plim = lim - i0;
-                switch (ah) {
-                    case 0: store_octets<0>(out_pass, v, lane, plim); break;
-                    case 1: store_octets<1>(out_pass, v, lane, plim); break;
-                    case 2: store_octets<2>(out_pass, v, lane, plim); break;
-                    default: store_octets<3>(out_pass, v, lane, plim); break;
+                    for (int k = 0; k < 4; ++k) {
+                        const int ii = i0 + k;
+                        if (ii >= 0 && static_cast<unsigned>(ii) < lim) stg_stream4(qbase + 4 * q + k, vals[ii] + carry);
+                    }
                 }
             }
             if (kTrace && tid == 0) P.trace[static_cast<unsigned long long>(t - kLag * G) * 8 + 6] = gtimer();
@@ -517,7 +515,6 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             dst[0] = make_uint4(val[p][0] + e, val[p][1] + e, val[p][2] + e, val[p][3] + e);
             dst[1] = make_uint4(val[p][4] + e, val[p][5] + e, val[p][6] + e, val[p][7] + e);
         }
-        tile_done_arrive();
     }
 
     // ---- completion; the last CTA produces the DecodeResult ----

@@ -15,6 +15,7 @@
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
 #include "decode_pipelined.cuh"
+#include "decode_warp.cuh"
 
 namespace {
 
@@ -34,6 +35,14 @@ size_t ws_need(size_t tiles) {
     return kHeaderBytes + (tiles * mvbk::kDescArrays + groups_for(tiles) * mvbk::kGroupArrays) * 8;
 }
 
+// Warp-tile kernel (decode_warp.cuh): header | count[n] | sum[n] | group count/sum [ng] x2 |
+// supergroup count/sum [ns] x2 | group accumulators [ng] x2 | supergroup accumulators [ns] x2.
+size_t wtiles_for(size_t mis, size_t scan_len) { return (mis + scan_len + mvbk::kWTile - 1) / mvbk::kWTile; }
+size_t ws_need_warp(size_t wtiles) {
+    const size_t ng = (wtiles + 31) / 32, ns = (ng + 31) / 32;
+    return kHeaderBytes + (2 * wtiles + 4 * ng + 4 * ns) * 8;
+}
+
 // Bytes the decode of `count` integers can touch: every integer (strict or
 // permissive) spans at most 5 bytes, so nothing past 5*count matters.
 size_t scan_length(size_t in_len, size_t count) {
@@ -41,7 +50,10 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
-int g_kernel_choice = 0;  // 0: pipelined for strict mode (default); 1: per-tile kernel (profiling only)
+// Strict-mode kernel: 0 CTA-pipelined (default), 1 per-tile kernel, 2 warp-tile kernel.
+// Permissive mode always runs the per-tile kernel (it needs a third lookback
+// component inside phase 1).  The switch exists for profiling comparisons.
+int g_kernel_choice = 0;
 
 template <bool Delta, int Mode>
 cudaError_t launch(const Params& p, cudaStream_t s) {
@@ -78,6 +90,33 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
 }
 
 template <bool Delta>
+cudaError_t launch_warp(const mvbk::WParams& w, unsigned n_wtiles, cudaStream_t s) {
+    static int per_sm = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 0) {
+        e = cudaFuncSetAttribute(mvbk::vbyte_decode_warp<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kWSmemBytes);
+        if (e != cudaSuccess) return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_warp<Delta>, mvbk::kWThreads,
+                                                          mvbk::kWSmemBytes);
+        if (e != cudaSuccess) return e;
+        per_sm = n > 0 ? n : 1;
+    }
+    // every warp must be resident (a lookback may wait on any earlier tile)
+    const long long cap = static_cast<long long>(per_sm) * sms;
+    const long long need = (static_cast<long long>(n_wtiles) + mvbk::kWWarps - 1) / mvbk::kWWarps;
+    const unsigned grid = static_cast<unsigned>(need < cap ? need : cap);
+    mvbk::vbyte_decode_warp<Delta><<<grid, mvbk::kWThreads, mvbk::kWSmemBytes, s>>>(w);
+    return cudaGetLastError();
+}
+
+template <bool Delta>
 cudaError_t launch_pipelined(const Params& p, cudaStream_t s) {
     return p.trace ? launch_pipelined_t<Delta, true>(p, s) : launch_pipelined_t<Delta, false>(p, s);
 }
@@ -99,8 +138,10 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
     const size_t scan = scan_length(in_len, count);
     const size_t tiles = tiles_for(mis, scan);
-    if (ws == nullptr || ws_bytes < ws_need(tiles)) return MVB_ERR_WORKSPACE;
-    if (tiles >= (1ull << 31)) return MVB_ERR_INVALID_ARG;
+    const bool warp_kernel = mode == MVB_STRICT && g_kernel_choice == 2 && trace == nullptr;
+    const size_t wtiles = wtiles_for(mis, scan);
+    if (ws == nullptr || ws_bytes < (warp_kernel ? ws_need_warp(wtiles) : ws_need(tiles))) return MVB_ERR_WORKSPACE;
+    if (wtiles >= (1ull << 40)) return MVB_ERR_INVALID_ARG;
 
     Params p;
     p.in = in;
@@ -123,7 +164,26 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.trace = trace;
 
     cudaError_t e;
-    if (mode == MVB_STRICT && g_kernel_choice == 0)
+    if (warp_kernel) {
+        mvbk::WParams w;
+        w.p = p;
+        w.p.n_tiles = static_cast<unsigned>(wtiles);
+        const size_t ng = (wtiles + 31) / 32, ns = (ng + 31) / 32;
+        w.n_groups = static_cast<long long>(ng);
+        w.n_super = static_cast<long long>(ns);
+        w.p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
+        w.p.dsum = w.p.dcnt + wtiles;
+        w.g1cnt = w.p.dsum + wtiles;
+        w.g1sum = w.g1cnt + ng;
+        w.g2cnt = w.g1sum + ng;
+        w.g2sum = w.g2cnt + ns;
+        w.a1cnt = w.g2sum + ns;
+        w.a1sum = w.a1cnt + ng;
+        w.a2cnt = w.a1sum + ng;
+        w.a2sum = w.a2cnt + ns;
+        e = delta ? launch_warp<true>(w, static_cast<unsigned>(wtiles), stream)
+                  : launch_warp<false>(w, static_cast<unsigned>(wtiles), stream);
+    } else if (mode == MVB_STRICT && (g_kernel_choice == 0 || trace != nullptr))
         e = delta ? launch_pipelined<true>(p, stream) : launch_pipelined<false>(p, stream);
     else if (delta)
         e = mode == MVB_STRICT ? launch<true, mvbk::MODE_STRICT>(p, stream)
@@ -203,7 +263,8 @@ inline size_t vb_size(uint32_t x) {
 extern "C" {
 
 size_t mvb_workspace_bytes(size_t in_len) {
-    return ws_need(tiles_for(15, in_len) + 1);
+    const size_t a = ws_need(tiles_for(15, in_len) + 1), b = ws_need_warp(wtiles_for(15, in_len) + 1);
+    return a > b ? a : b;
 }
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
@@ -277,8 +338,7 @@ int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta
     return decode_device(in, in_len, count, delta != 0, prev, out, mode, res_dev, ws, ws_bytes, stream, trace);
 }
 
-// Internal profiling switch (not part of include/mvb_cuda.h): 0 = pipelined
-// strict-mode kernel (default), 1 = per-tile kernel for every mode.
+// Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
 const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }

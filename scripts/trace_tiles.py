@@ -44,6 +44,7 @@ for it in range(8):
     times.append(s.elapsed_time(e) * 1e3)
 expected = torch.from_numpy(w.expected().view(np.int32)).to(dev)
 assert torch.equal(out, expected), "mismatch"
+print("grid", L.mvbx_last_grid() if hasattr(L, "mvbx_last_grid") else "?")
 for it in range(3):
     flush.fill_(it)
     torch.cuda.synchronize()

@@ -281,3 +281,44 @@ def test_config4_full_size_device(golden, oracle, cuda):
                                                                   s["bytes_consumed"])
     got = out.cpu().numpy().view(np.uint32)
     assert oracle.fnv_u32(got) == s["out_fnv"]
+
+
+@pytest.mark.parametrize("choice", [1, 2, 0])
+def test_every_strict_kernel_variant(choice, golden, oracle):
+    """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined) agree with
+    the oracle on KATs, errors across tile boundaries and a full config."""
+    from paper_1503_07387_b200 import _lib
+
+    _lib.set_kernel_choice(choice)
+    try:
+        kat, sums = golden
+        for c in kat:
+            if c["mode"] != STRICT:
+                continue
+            data = np.frombuffer(bytes.fromhex(c["bytes"]), np.uint8)
+            check_case(c, gpu_decode(data, c["count"], c["mode"], c["delta"], c["prev"]))
+        v = W.mixed_values(70000, 8)
+        enc = oracle.encode_sequence(v)
+        for pos in (0, 511, 512, 513, 4095, 4096, 9000, 40001):
+            data = _inject(enc, pos, [0x80] * 6)
+            for count in (v.size, 5000):
+                ro, oo = oracle.decode(data, count)
+                r, out = gpu_decode(data, count)
+                assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (choice, pos, count)
+                ro, oo = oracle.decode_delta(data, count, 3)
+                r, out = gpu_decode(data, count, delta=True, prev=3)
+                assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (choice, pos, count)
+        for n in (1, 3, 600, 100001):
+            w = W.mixed_values(n, n + 1)
+            e = oracle.encode_sequence(w)
+            for cut in (e.size, max(1, e.size - 3)):
+                ro, oo = oracle.decode(e[:cut], n)
+                r, out = gpu_decode(e[:cut], n)
+                assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (choice, n, cut)
+        s = sums["config2"]
+        w = W.config2()
+        r, out = gpu_decode(w.encoded, w.count, delta=True)
+        assert r == (s["status"], s["values_written"], s["bytes_consumed"])
+        assert oracle.fnv_u32(out) == s["out_fnv"]
+    finally:
+        _lib.set_kernel_choice(0)
