@@ -54,7 +54,8 @@ def load_ncu_traffic(workload):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(workload)
+        v = d.get(workload)
+        return float(v) if v is not None else None
     except Exception:
         return None
 
