@@ -94,6 +94,15 @@ int mvb_decode_delta_device(const uint8_t *in, size_t in_len, size_t count, uint
                             uint32_t *out, int mode, mvb_result *res_dev, void *ws,
                             size_t ws_bytes, mvb_stream_t stream);
 
+/* Sharded-decode pre-pass: number of integers that END in
+ * in[0..in_len) (terminator bytes) and the sum of their values mod 2^32,
+ * written to device memory.  A shard of a longer stream, cut at integer
+ * boundaries, is decoded with prev = the caller's running sum of the earlier
+ * shards' totals -- the per-shard split of decode_delta_scalar's
+ * `prev += value` (vbyte.cpp:63-74).  Asynchronous on `stream`. */
+int mvb_scan_totals_device(const uint8_t *in, size_t in_len, unsigned long long *count_dev,
+                           uint32_t *sum_dev, mvb_stream_t stream);
+
 /* ------------------------------------------------------------ host drop-ins */
 
 /* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream

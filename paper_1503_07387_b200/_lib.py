@@ -19,6 +19,7 @@ EXPORTS = (
     "mvb_workspace_init",
     "mvb_decode_device",
     "mvb_decode_delta_device",
+    "mvb_scan_totals_device",
     "mvb_decode_stream",
     "mvb_decode_delta_stream",
     "mvb_encoded_size",
@@ -58,6 +59,8 @@ def _declare(lib):
     lib.mvb_decode_device.restype = i32
     lib.mvb_decode_delta_device.argtypes = [vp, sz, sz, u32, vp, i32, vp, vp, sz, vp]
     lib.mvb_decode_delta_device.restype = i32
+    lib.mvb_scan_totals_device.argtypes = [vp, sz, vp, vp, vp]
+    lib.mvb_scan_totals_device.restype = i32
     lib.mvb_decode_stream.argtypes = [vp, sz, sz, vp, i32, ctypes.POINTER(MvbResult)]
     lib.mvb_decode_stream.restype = i32
     lib.mvb_decode_delta_stream.argtypes = [vp, sz, sz, u32, vp, i32, ctypes.POINTER(MvbResult)]

@@ -16,6 +16,7 @@
 #include "decode_kernel.cuh"
 #include "decode_pipelined.cuh"
 #include "decode_warp.cuh"
+#include "totals_kernel.cuh"
 
 namespace {
 
@@ -289,6 +290,26 @@ int mvb_decode_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t* 
 int mvb_decode_delta_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t prev, uint32_t* out,
                             int mode, mvb_result* res) {
     return decode_host(in, in_len, count, true, prev, out, mode, res);
+}
+
+int mvb_scan_totals_device(const uint8_t* in, size_t in_len, unsigned long long* count_dev, uint32_t* sum_dev,
+                           mvb_stream_t stream) {
+    if ((in == nullptr && in_len > 0) || count_dev == nullptr || sum_dev == nullptr) return MVB_ERR_INVALID_ARG;
+    if (cudaMemsetAsync(count_dev, 0, sizeof(unsigned long long), stream) != cudaSuccess ||
+        cudaMemsetAsync(sum_dev, 0, sizeof(uint32_t), stream) != cudaSuccess)
+        return MVB_ERR_CUDA;
+    if (in_len == 0) return 0;
+    const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
+    const size_t tiles = tiles_for(mis, in_len);
+    if (tiles >= (1ull << 32)) return MVB_ERR_INVALID_ARG;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(sms) * 8));
+    mvbk::vbyte_totals_kernel<<<grid, mvbk::kThreads, 0, stream>>>(in, static_cast<long long>(mis),
+                                                                   static_cast<long long>(in_len),
+                                                                   static_cast<unsigned>(tiles), count_dev, sum_dev);
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
 size_t mvb_encoded_size(uint32_t x) { return vb_size(x); }
