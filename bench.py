@@ -11,8 +11,12 @@ timed region.  L2 residency is defeated by rotating 4 input/output buffer
 sets whose total (4 x 92 MB for c2) is well above the 126 MB L2.
 
 Multi-GPU (torchrun): configs c1/c2/c5 are independent replicas per rank
-(weak scaling, no data-path collective); timing is CUDA events
-with barrier + synchronize on both sides and the max over ranks.
+(weak scaling, no data-path collective).  --config c4 is the
+sharded config: one 2^30-integer delta stream split by byte range across the
+ranks (strong scaling): per step a totals pre-pass, one NCCL all-gather of a
+16-byte record per rank, a carry kernel and the decode, all on-stream.
+Timing is CUDA events with barrier + synchronize on both sides and the max
+over ranks.
 
 --impl reference times the reference's own CPU decoder (oracle/_ref, the
 unmodified reference library built from its sources) on this host's cores:
@@ -180,6 +184,11 @@ def run_reference(args):
     if rank != 0:
         return
     w = make_workload(args.config)
+    if w.count > (1 << 26):  # bounded sample per thread: the first 2^26 integers of the stream
+        from paper_1503_07387_b200 import workload as W
+
+        k = 1 << 26
+        w = W.Workload(w.name, w.delta, w.values[:k], w.encoded[:int(W.encode(w.values[:k]).size)], prev=w.prev)
     threads = os.cpu_count() or 1
     # each step: every host thread decodes one replica (bounded: ~ a few s total)
     rates = []
@@ -358,6 +367,172 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _check_shard_values(torch, dev, vals, gaps, offset, prev):
+    """Device-side check of a shard's delta output against the ground-truth
+    gaps: out[i] = prev + gaps[0] + ... + gaps[offset + i] (mod 2^32)."""
+    carry = (prev + int(gaps[:offset].astype(np.uint64).sum())) & 0xFFFFFFFF
+    step = 1 << 26
+    for a in range(0, vals.numel(), step):
+        g = torch.from_numpy(gaps[offset + a: offset + a + min(step, vals.numel() - a)].astype(np.int64)).to(dev)
+        exp = (torch.cumsum(g, 0) + carry) & 0xFFFFFFFF
+        got = vals[a:a + g.numel()].to(torch.int64) & 0xFFFFFFFF
+        if not torch.equal(got, exp):
+            return False
+        carry = int(exp[-1].item())
+    return True
+
+
+def run_sharded(args):
+    """Config 4: one 2^30-integer delta stream split by byte range across the
+    ranks (strong scaling).  A step is one pass of
+    DeviceShard.run() on every rank: totals pre-pass, NCCL all-gather of a
+    16-byte record, carry kernel, decode with the device-resident carry."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_07387_b200 import shard as S
+
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    w = make_workload(args.config)
+    L = int(w.encoded.size)
+    lo, hi = S.local_range(L, world, rank)
+    h_buf = torch.from_numpy(w.encoded[lo:hi]).pin_memory()
+    buf = h_buf.to(dev)
+    sh = S.DeviceShard(buf, lo, L, w.delta, w.prev, world, rank)
+    stream = torch.cuda.current_stream(dev)
+
+    # correctness gate: whole-stream result and this rank's slice of the values
+    sh.run()
+    off, vals, glob = sh.result()
+    assert glob == (0, w.count, L), glob
+    if w.delta:
+        assert _check_shard_values(torch, dev, vals, w.values, off, w.prev), "sharded decode mismatch"
+    else:
+        assert torch.equal(vals, torch.from_numpy(w.values[off:off + vals.numel()].view(np.int32)).to(dev))
+    n_local = int(vals.numel())
+    del vals
+
+    for _ in range(max(args.warmup, 3)):
+        sh.run()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < args.preroll:
+        for _ in range(8):
+            sh.run()
+        torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for s in range(args.steps):
+            sh.prepass()
+            if w.delta and world > 1:
+                sh.exchange()
+            ev[s][0].record(stream)
+            sh.decode()
+            ev[s][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(stop)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    _, _, glob = sh.result()
+    assert glob == (0, w.count, L), glob
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = w.count * args.steps / (total_ms / 1e3) / 1e9
+
+    shard_bytes = sh.bound
+    alg_bytes = shard_bytes + 4 * n_local
+    achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+
+    # end to end: H2D of this rank's byte range from pinned memory, the pass,
+    # D2H of its decoded integers, every step
+    h_out = torch.empty(max(sh.bound, 1), dtype=torch.int32).pin_memory()
+
+    def e2e_step():
+        buf.copy_(h_buf, non_blocking=True)
+        sh.run()
+        h_out[:n_local].copy_(sh.out[:n_local], non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e_steps = max(3, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_dt = time.perf_counter() - t0
+    et = torch.tensor([e_dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = w.count * e_steps / float(et.item()) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        try:
+            rate, reps, sample = cpu_reference_sample(w, args.cpu_seconds, 1)
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.count, "in_bytes": L, "bytes_per_int": round(w.bytes_per_int, 4),
+                       "delta": w.delta, "parallelism": f"byte-range shards x{world}" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 (rank 0 shard {shard_bytes / 1e6:.0f} MB in + "
+                             f"{4 * n_local / 1e6:.0f} MB out > 126 MB)"},
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": load_ncu_traffic(w.name), "peak_kind": peak_kind,
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": statistics.mean(kern_ms),
+                         "kernel_ms_min": min(kern_ms), "kernel": "decode of rank 0's shard"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_buf.numel()),
+                    "d2h_bytes_per_step": 4 * n_local,
+                    "api": "DeviceShard.run (pre-pass, all-gather, carry, decode) with pinned H2D/D2H"},
+            "gpu_launches": args.steps * sh.launches_per_pass,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_reference_sample(w, seconds, threads):
+    """Reference decode rate on a bounded prefix of a large stream (2^26
+    integers, the reference's l1-style chunk of the same bytes)."""
+    from paper_1503_07387_b200 import workload as W
+
+    k = min(w.count, 1 << 26)
+    sub = W.Workload(w.name, w.delta, w.values[:k], w.encoded[:int(W.encode(w.values[:k]).size)], prev=w.prev)
+    rate, reps = cpu_reference_rate(sub, seconds, threads)
+    return rate, reps, (f"{reps} decodes of the first {k} integers of the {w.name} stream by the reference "
+                        f"library's decode{'_delta' if w.delta else ''}_stream (SSE masked path), "
+                        f"{threads} thread(s), ~{seconds:.0f} s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,6 +545,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4":
+        run_sharded(args)
     else:
         run_ours(args)
 

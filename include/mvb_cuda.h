@@ -103,6 +103,23 @@ int mvb_decode_delta_device(const uint8_t *in, size_t in_len, size_t count, uint
 int mvb_scan_totals_device(const uint8_t *in, size_t in_len, unsigned long long *count_dev,
                            uint32_t *sum_dev, mvb_stream_t stream);
 
+/* mvb_decode_delta_device with the starting value read from device memory
+ * when the kernel runs (prev = *prev_dev), so a carry computed on the device
+ * (mvb_shard_carry_device) feeds the decode without a host round trip. */
+int mvb_decode_delta_device_dprev(const uint8_t *in, size_t in_len, size_t count,
+                                  const uint32_t *prev_dev, uint32_t *out, int mode,
+                                  mvb_result *res_dev, void *ws, size_t ws_bytes,
+                                  mvb_stream_t stream);
+
+/* Seam fix-up of the sharded decode: from n_ranks all-gathered records of
+ * record_words u64 each (word 0 = integer count, low 32 bits of word 1 = gap
+ * sum, as written by mvb_scan_totals_device), writes shard `rank`'s carry-in
+ * prev + sum[0..rank) mod 2^32 and its output offset count[0..rank).  Either
+ * output may be NULL.  Asynchronous on `stream`. */
+int mvb_shard_carry_device(const unsigned long long *records, int n_ranks, int rank,
+                           int record_words, uint32_t prev, uint32_t *carry_dev,
+                           unsigned long long *offset_dev, mvb_stream_t stream);
+
 /* ------------------------------------------------------------ host drop-ins */
 
 /* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream

@@ -110,6 +110,7 @@ struct Params {
     unsigned long long count;  // integers requested
     uint32_t* out;
     uint32_t prev;
+    const uint32_t* prev_dev;  // optional: starting value added from device memory (sharded carry)
     unsigned n_tiles;
     WsHeader* hdr;
     unsigned long long* dcnt;  // per-tile count descriptors
@@ -123,6 +124,12 @@ struct Params {
     mvb_result* res_dev;       // optional
     unsigned long long* trace; // optional per-tile timeline (profiling only): 8 x u64 per tile
 };
+
+// Starting value of the delta scan: the host argument, plus the device-resident
+// carry when the caller passes one (written by an earlier kernel on the stream).
+__device__ __forceinline__ uint32_t prev_of(const Params& P) {
+    return P.prev_dev ? P.prev + *P.prev_dev : P.prev;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -810,10 +817,10 @@ __global__ void __launch_bounds__(kThreads, 5) vbyte_decode_kernel(Params P) {
         if (kDelta && lane == 0) {
             MVB_TRACE(4);
             publish_aggregate<true>(P.dsum, P.gsum, P.gacc_sum, t, P.n_tiles,
-                                    t == 0 ? static_cast<uint32_t>(P.prev + tile_sum) : tile_sum, epoch);
+                                    t == 0 ? static_cast<uint32_t>(prev_of(P) + tile_sum) : tile_sum, epoch);
         }
         unsigned long long c = 0;
-        uint32_t cs = P.prev;
+        uint32_t cs = prev_of(P);
         if (t > 0) {
             if (kDelta) {
                 lookback2_cnt_sum(P, t, epoch, lane, &c, &cs);

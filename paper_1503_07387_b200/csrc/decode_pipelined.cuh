@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
                 const int ps = (i - kLag) & 3;
                 const unsigned nt = s_ntile[ps];
                 unsigned long long c = 0;
-                uint32_t cs = P.prev;
+                uint32_t cs = prev_of(P);
                 if (tp > 0) {
                     if (kDelta) {
                         lookback2_cnt_sum(P, tp, epoch, lane, &c, &cs);
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             if (tid == 0) {
                 if (kTrace) P.trace[static_cast<unsigned long long>(t) * 8 + 4] = gtimer();
                 publish_aggregate<true>(P.dsum, P.gsum, P.gacc_sum, t, P.n_tiles,
-                                        t == 0 ? static_cast<uint32_t>(P.prev + tile_sum) : tile_sum, epoch);
+                                        t == 0 ? static_cast<uint32_t>(prev_of(P) + tile_sum) : tile_sum, epoch);
                 s_tsum[i & 3] = tile_sum;
             }
         }

@@ -512,13 +512,13 @@ __global__ void __launch_bounds__(kWThreads, 3) vbyte_decode_warp(WParams W) {
             tile_sum = carry_in;
             if (kDelta && lane == 0)
                 lb3_publish_agg<true>(P.dsum, W.g1sum, W.g2sum, W.a1sum, W.a2sum, t, nt,
-                                      t == 0 ? static_cast<uint32_t>(P.prev + tile_sum) : tile_sum, epoch);
+                                      t == 0 ? static_cast<uint32_t>(prev_of(P) + tile_sum) : tile_sum, epoch);
         }
 
         // ---- resolve and store t_{i-2} ----
         if (tl1 >= 0) {
             unsigned long long cnt_prefix = 0;
-            uint32_t carry = P.prev;
+            uint32_t carry = prev_of(P);
             if (have_prev) {
                 cnt_prefix = lb3_resolve<false>(lc, P.dcnt, W.g1cnt, W.g2cnt, tp, epoch, lane);
                 if (kDelta) carry = static_cast<uint32_t>(lb3_resolve<true>(ls, P.dsum, W.g1sum, W.g2sum, tp, epoch, lane));

@@ -124,7 +124,8 @@ cudaError_t launch_pipelined(const Params& p, cudaStream_t s) {
 
 int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
                   uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
-                  cudaStream_t stream, unsigned long long* trace = nullptr) {
+                  cudaStream_t stream, unsigned long long* trace = nullptr,
+                  const uint32_t* prev_dev = nullptr) {
     if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
     if (mode != MVB_STRICT && mode != MVB_PERMISSIVE) return MVB_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
@@ -151,6 +152,7 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.count = count;
     p.out = out;
     p.prev = prev;
+    p.prev_dev = prev_dev;
     p.n_tiles = static_cast<unsigned>(tiles);
     p.hdr = static_cast<WsHeader*>(ws);
     p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
@@ -281,6 +283,23 @@ int mvb_decode_device(const uint8_t* in, size_t in_len, size_t count, uint32_t* 
 int mvb_decode_delta_device(const uint8_t* in, size_t in_len, size_t count, uint32_t prev, uint32_t* out,
                             int mode, mvb_result* res_dev, void* ws, size_t ws_bytes, mvb_stream_t stream) {
     return decode_device(in, in_len, count, true, prev, out, mode, res_dev, ws, ws_bytes, stream);
+}
+
+int mvb_decode_delta_device_dprev(const uint8_t* in, size_t in_len, size_t count, const uint32_t* prev_dev,
+                                  uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
+                                  mvb_stream_t stream) {
+    if (prev_dev == nullptr) return MVB_ERR_INVALID_ARG;
+    return decode_device(in, in_len, count, true, 0, out, mode, res_dev, ws, ws_bytes, stream, nullptr, prev_dev);
+}
+
+int mvb_shard_carry_device(const unsigned long long* records, int n_ranks, int rank, int record_words,
+                           uint32_t prev, uint32_t* carry_dev, unsigned long long* offset_dev,
+                           mvb_stream_t stream) {
+    if (records == nullptr || n_ranks < 1 || rank < 0 || rank >= n_ranks || record_words < 2 ||
+        (carry_dev == nullptr && offset_dev == nullptr))
+        return MVB_ERR_INVALID_ARG;
+    mvbk::shard_carry_kernel<<<1, 32, 0, stream>>>(records, rank, record_words, prev, carry_dev, offset_dev);
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
 int mvb_decode_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t* out, int mode, mvb_result* res) {

@@ -64,6 +64,15 @@ __global__ void __launch_bounds__(kThreads) vbyte_totals_kernel(const uint8_t* i
         }
         uint32_t ends = T16 & inr16;
         cnt += __popc(ends);
+        // single-byte integers (terminator preceded by a terminator; bytes
+        // before the range read as 0x00, a terminator): the byte is the value
+        const uint32_t single = ends & (Tx >> 7);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t m = (single >> (4 * k)) & 0xFu;
+            sum = __dp4a(w[k] & (((m * 0x204081u) & 0x01010101u) * 0xFFu), 0x01010101u, sum);
+        }
+        ends &= ~single;
         const uint32_t d[6] = {digits4(wp2), digits4(wp3), digits4(w[0]), digits4(w[1]), digits4(w[2]), digits4(w[3])};
         while (ends) {
             const int j = __ffs(ends) - 1;
@@ -90,6 +99,28 @@ __global__ void __launch_bounds__(kThreads) vbyte_totals_kernel(const uint8_t* i
         }
         atomicAdd(count_out, c);
         atomicAdd(sum_out, s);
+    }
+}
+
+// Carry-in and output offset of shard `rank` from the all-gathered per-shard
+// records (word 0 = integer count, low half of word 1 = gap sum mod 2^32):
+// the exclusive scans that stitch the shards' decodes together.
+__global__ void shard_carry_kernel(const unsigned long long* rec, int rank, int words, uint32_t prev,
+                                   uint32_t* carry, unsigned long long* offset) {
+    unsigned long long c = 0;
+    uint32_t s = 0;
+    for (int h = threadIdx.x; h < rank; h += 32) {
+        c += rec[static_cast<long long>(h) * words];
+        s += static_cast<uint32_t>(rec[static_cast<long long>(h) * words + 1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    }
+    if (threadIdx.x == 0) {
+        if (carry) *carry = prev + s;
+        if (offset) *offset = c;
     }
 }
 

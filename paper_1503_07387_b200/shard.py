@@ -239,3 +239,115 @@ def sharded_decode(buf, buf_lo: int, total_len: int, count: int, delta: bool, pr
     local, values = ops.decode(shard, want[rank], carry if delta else 0, delta, out)
     status_recs = gather([local[0], local[1], local[2], plan.start, want[rank]])
     return offset, values, combine_results(status_recs)
+
+
+class DeviceShard:
+    """One rank's shard, decoded with no host round trip (bench / device-resident path).
+
+    Every pass queues, on the current stream: the totals pre-pass (delta, all
+    ranks but the last -- nobody needs the last shard's sum), an all-gather of
+    a 16-byte record {count, gap sum} per rank, the carry kernel, and the
+    decode with its starting value read from device memory.  Plain decode
+    needs no exchange at all: each shard decodes independently and only the
+    output offsets (metadata, ``result()``) use the gathered counts.
+
+    The shard is decoded with ``count`` = its byte length (an upper bound on
+    its integers), i.e. "every integer in the stream": a shard that ends
+    cleanly reports truncated with all bytes consumed, which ``result()``
+    reads as OK -- the whole-stream decode with count = number of integers.
+    """
+
+    RECORD_WORDS = 2
+
+    def __init__(self, buf, buf_lo: int, total_len: int, delta: bool, prev: int = 0,
+                 world: int = 1, rank: int = 0, group=None, gather=None):
+        import torch
+
+        from . import _lib, mvb
+
+        self.torch = torch
+        self.lib = _lib.lib()
+        self.device = buf.device
+        self.delta, self.prev = delta, prev & 0xFFFFFFFF
+        self.world, self.rank, self.group = world, rank, group
+        self.total_len = total_len
+        cuts = shard_cuts(total_len, world)
+        self.plan = plan_shard(_window_view(buf, buf_lo, total_len, cuts, rank), buf_lo, total_len, world, rank)
+        self.shard = buf[self.plan.start - buf_lo: self.plan.end - buf_lo]
+        self.bound = int(self.shard.numel())
+        self.out = torch.empty(max(self.bound, 1), dtype=torch.int32, device=self.device)
+        self.rec = torch.zeros(self.RECORD_WORDS, dtype=torch.int64, device=self.device)
+        self.recs = torch.zeros(world * self.RECORD_WORDS, dtype=torch.int64, device=self.device)
+        self.carry = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.dec = mvb.Decoder(self.device, capacity_bytes=max(self.bound, 1))
+        self.gather = gather
+        self.launches_per_pass = 1 + (2 if delta and world > 1 and rank < world - 1 else
+                                      1 if delta and world > 1 else 0)
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def prepass(self):
+        """Totals of this shard into the local record (delta, not the last rank)."""
+        if not self.delta or self.world == 1 or self.rank == self.world - 1:
+            return
+        n = self.bound
+        rc = self.lib.mvb_scan_totals_device(self.shard.data_ptr() if n else None, n, self.rec.data_ptr(),
+                                             self.rec.data_ptr() + 8, self._stream())
+        if rc != 0:
+            raise RuntimeError(f"mvb_scan_totals_device failed ({rc})")
+
+    def exchange(self):
+        """All-gather of the records (the only collective)."""
+        if self.gather is not None:
+            self.gather(self.recs, self.rec)
+        else:
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.recs, self.rec, group=self.group)
+
+    def decode(self):
+        n, s = self.bound, self._stream()
+        self.dec._ensure(max(n, 1))
+        ws, wsb = self.dec.ws.data_ptr(), self.dec.ws_bytes
+        if self.delta and self.world > 1:
+            rc = self.lib.mvb_shard_carry_device(self.recs.data_ptr(), self.world, self.rank, self.RECORD_WORDS,
+                                                 self.prev, self.carry.data_ptr(), None, s)
+            if rc != 0:
+                raise RuntimeError(f"mvb_shard_carry_device failed ({rc})")
+            rc = self.lib.mvb_decode_delta_device_dprev(self.shard.data_ptr() if n else None, n, n,
+                                                        self.carry.data_ptr(), self.out.data_ptr() if n else None,
+                                                        0, self.dec.res.data_ptr(), ws, wsb, s)
+        elif self.delta:
+            rc = self.lib.mvb_decode_delta_device(self.shard.data_ptr() if n else None, n, n, self.prev,
+                                                  self.out.data_ptr() if n else None, 0, self.dec.res.data_ptr(),
+                                                  ws, wsb, s)
+        else:
+            rc = self.lib.mvb_decode_device(self.shard.data_ptr() if n else None, n, n,
+                                            self.out.data_ptr() if n else None, 0, self.dec.res.data_ptr(),
+                                            ws, wsb, s)
+        if rc != 0:
+            raise RuntimeError(f"shard decode failed ({rc})")
+
+    def run(self):
+        """One pass over the shard (queued on the current stream)."""
+        self.prepass()
+        if self.delta and self.world > 1:
+            self.exchange()
+        self.decode()
+
+    def local_result(self) -> List[int]:
+        """(status, written, consumed, start, requested) with a clean end read as OK."""
+        r = self.dec.result()
+        status = int(r.status)
+        if status == 1 and r.bytes_consumed == self.bound:
+            status = 0
+        return [status, int(r.values_written), int(r.bytes_consumed), self.plan.start, self.bound]
+
+    def result(self, gather_records=None):
+        """(global_offset, values, whole-stream DecodeResult); synchronises."""
+        gather = gather_records or (lambda rec: _all_gather_records(rec, self.group))
+        recs = gather(self.local_result()) if self.world > 1 else [self.local_result()]
+        offset = sum(r[1] for r in recs[:self.rank])
+        mine = recs[self.rank]
+        return offset, self.out[:mine[1]], combine_results(recs)

@@ -296,3 +296,51 @@ def test_sharded_cuda_equals_whole_stream(cuda, world):
     bad = np.concatenate([bad[:q], np.full(40, 0x90, np.uint8), bad[q:]])
     check_against_whole(bad, gaps.size, world, True, ops_for_rank=lambda g: ops[g], to_buf=to_buf)
     check_against_whole(enc[:-1], gaps.size, world, True, ops_for_rank=lambda g: ops[g], to_buf=to_buf)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_device_shards_equal_whole_stream(cuda, world):
+    """DeviceShard phases (pre-pass -> record exchange -> carry -> decode) for W
+    virtual shards on one GPU; the exchange is a device copy standing in for
+    the NCCL all-gather."""
+    import torch
+
+    gaps = W.mixed_values(2_000_000, world + 70)
+    for data in (oracle().encode_sequence(gaps), None):
+        if data is None:  # malformed: an over-long run in the middle
+            enc = oracle().encode_sequence(gaps)
+            q = S.resync(enc, 0, enc.size // 2 + 5, enc.size)[0]
+            data = np.concatenate([enc[:q], np.full(30, 0x88, np.uint8), enc[q:]])
+        L = data.size
+        n_ints = int((data < 0x80).sum())
+        for delta in (False, True):
+            shards = []
+            for g in range(world):
+                lo, hi = S.local_range(L, world, g)
+                shards.append(S.DeviceShard(torch.from_numpy(data[lo:hi].copy()).to(cuda), lo, L, delta,
+                                            prev=0xFFFFFFF0, world=world, rank=g))
+            recs_all = torch.zeros(world * 2, dtype=torch.int64, device=cuda)
+            for sh in shards:
+                sh.prepass()
+            for g, sh in enumerate(shards):
+                recs_all[2 * g:2 * g + 2] = sh.rec
+            for sh in shards:
+                sh.recs.copy_(recs_all)
+                sh.decode()
+            torch.cuda.synchronize()
+            locs = [sh.local_result() for sh in shards]
+            got = np.zeros(n_ints, np.uint32)
+            off = 0
+            for sh, lr in zip(shards, locs):
+                v = sh.out[:lr[1]].cpu().numpy().view(np.uint32)
+                got[off:off + v.size] = v
+                off += v.size
+            glob = S.combine_results(locs)
+            if delta:
+                want_r, want = oracle().decode_delta(data, n_ints, 0xFFFFFFF0, STRICT)
+            else:
+                want_r, want = oracle().decode(data, n_ints, STRICT)
+            assert glob == tuple(want_r), (world, delta, glob, want_r)
+            k = want_r[1]
+            np.testing.assert_array_equal(got[:k], want[:k])
