@@ -75,6 +75,17 @@ __device__ __forceinline__ void workers_sync() {
 }
 
 
+// Bank-conflict swizzles (scripts/smem_model.py).  V holds one word per byte
+// position; worker t stores its 16 words as four 16-byte chunks at a 64-byte
+// stride, which without a swizzle puts 16 lanes on the same 4 banks.  XOR-ing
+// word-address bits 2-3 with bits 5-6 keeps 16-byte chunks intact and spreads
+// the 8 lanes of each wavefront over all 8 chunk slots.  VAL (parked values,
+// two 16-byte chunks per lane) uses the 3-bit XOR of the chunk index with its
+// 128-byte row, which keeps both the park stores and the copy-out's
+// consecutive-chunk loads conflict-free.
+__device__ __forceinline__ uint32_t v_swz(uint32_t byte_off) { return byte_off ^ ((byte_off >> 3) & 0x30u); }
+__device__ __forceinline__ uint32_t val_chunk(uint32_t c) { return c ^ ((c >> 3) & 7u); }
+
 // Tile geometry helpers.
 __device__ __forceinline__ long long tile_pos0(const Params& P, long long t) { return t * kTile - P.mis; }
 // Interior tiles: the whole buffer [tpos0-16, tpos0+4096+16) lies inside the stream.
@@ -318,10 +329,16 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             }
             if (kTrace && tid == 0) P.trace[static_cast<unsigned long long>(t) * 8 + 0] = gtimer();
             const uint4 q = *reinterpret_cast<const uint4*>(buf + lp0);
-            const uint2 pv = *reinterpret_cast<const uint2*>(buf + lp0 - 8);
             w0 = q.x; w1 = q.y; w2 = q.z; w3 = q.w;
-            wp2 = pv.x; wp3 = pv.y;
-            wn = *reinterpret_cast<const uint32_t*>(buf + lp0 + kChunk);
+            // halo words from the neighbouring lanes (strided loads would hit 2 banks)
+            wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1);
+            wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
+            wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
+            if (lane == 0) {
+                const uint2 pv = *reinterpret_cast<const uint2*>(buf + lp0 - 8);
+                wp2 = pv.x; wp3 = pv.y;
+            }
+            if (lane == 31) wn = *reinterpret_cast<const uint32_t*>(buf + lp0 + kChunk);
 
             const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
             Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
@@ -365,35 +382,46 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             const uint32_t carry = kDelta ? s_sum_pre[ps] : 0u;
             const unsigned long long room = P.count > cnt_prefix ? P.count - cnt_prefix : 0ull;
             const unsigned lim = room < ntile_lag1 ? static_cast<unsigned>(room) : ntile_lag1;
-            // quad q covers tile-local ints 4q-a .. 4q-a+3 at a 16-byte-aligned address
+            // head: h ints up to the first 16-byte-aligned output address,
+            // body: aligned quads, tail: the rest (h, tail stored singly)
             const unsigned a = static_cast<unsigned>(((reinterpret_cast<uintptr_t>(P.out) >> 2) + cnt_prefix) & 3u);
-            uint32_t* const qbase = P.out + cnt_prefix - a;
-            const uint32_t* vals = VAL[cb];  // (i - 2) & 1 == i & 1
-            const unsigned nq = lim ? (lim + a + 3) >> 2 : 0u;
-            for (unsigned q = tid; q < nq; q += kPWorkerThreads) {
-                const int i0 = static_cast<int>(4 * q) - static_cast<int>(a);
-                if (i0 >= 0 && static_cast<unsigned>(i0) + 4 <= lim) {
-                    uint32_t v0, v1, v2, v3;
-                    if (a == 0) {
-                        const uint4 x = *reinterpret_cast<const uint4*>(vals + i0);
-                        v0 = x.x; v1 = x.y; v2 = x.z; v3 = x.w;
-                    } else if (a == 2) {
-                        const uint2 x = *reinterpret_cast<const uint2*>(vals + i0);
-                        const uint2 y = *reinterpret_cast<const uint2*>(vals + i0 + 2);
-                        v0 = x.x; v1 = x.y; v2 = y.x; v3 = y.y;
-                    } else {  // i0 odd: i0+1 is 8-byte aligned
-                        const uint2 x = *reinterpret_cast<const uint2*>(vals + i0 + 1);
-                        v0 = vals[i0]; v1 = x.x; v2 = x.y; v3 = vals[i0 + 3];
-                    }
-                    stg_stream16(qbase + 4 * q, v0 + carry, v1 + carry, v2 + carry, v3 + carry);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int ii = i0 + k;
-                        if (ii >= 0 && static_cast<unsigned>(ii) < lim) stg_stream4(qbase + 4 * q + k, vals[ii] + carry);
-                    }
-                }
+            const unsigned h = (4u - a) & 3u;
+            const uint4* vq = reinterpret_cast<const uint4*>(VAL[cb]);  // (i - 2) & 1 == i & 1
+            const uint32_t* vs = VAL[cb];
+            uint32_t* const o = P.out + cnt_prefix;
+            const unsigned hh = h < lim ? h : lim;
+            const unsigned nbody = (lim - hh) >> 2;
+            const unsigned tail0 = hh + 4 * nbody;
+            if (tid < hh) {
+                const unsigned i0 = tid;
+                stg_stream4(o + i0, vs[4 * val_chunk(i0 >> 2) + (i0 & 3)] + carry);
+            } else if (tid >= 4 && tid - 4 < lim - tail0) {
+                const unsigned i0 = tail0 + tid - 4;
+                stg_stream4(o + i0, vs[4 * val_chunk(i0 >> 2) + (i0 & 3)] + carry);
             }
+            // body quad m covers tile ints h + 4m .. h + 4m + 3: chunks m, m+1 when h > 0
+#define MVB_BODY(H)                                                                                   \
+    for (unsigned m = tid; m < nbody; m += kPWorkerThreads) {                                         \
+        uint4 x = vq[val_chunk(m)];                                                                   \
+        uint32_t r0, r1, r2, r3;                                                                      \
+        if (H == 0) {                                                                                 \
+            r0 = x.x; r1 = x.y; r2 = x.z; r3 = x.w;                                                   \
+        } else {                                                                                      \
+            const uint4 y = vq[val_chunk(m + 1)];                                                     \
+            if (H == 1) { r0 = x.y; r1 = x.z; r2 = x.w; r3 = y.x; }                                   \
+            else if (H == 2) { r0 = x.z; r1 = x.w; r2 = y.x; r3 = y.y; }                              \
+            else { r0 = x.w; r1 = y.x; r2 = y.y; r3 = y.z; }                                          \
+        }                                                                                             \
+        stg_stream16(o + hh + 4 * m, r0 + carry, r1 + carry, r2 + carry, r3 + carry);                 \
+    }
+            // h < lim implies hh == h; otherwise nbody == 0 and the body is empty
+            switch (h) {
+                case 0: MVB_BODY(0) break;
+                case 1: MVB_BODY(1) break;
+                case 2: MVB_BODY(2) break;
+                default: MVB_BODY(3) break;
+            }
+#undef MVB_BODY
             if (kTrace && tid == 0) P.trace[static_cast<unsigned long long>(t - kLag * G) * 8 + 6] = gtimer();
         }
         ntile_lag1 = ntile_lag0;
@@ -417,16 +445,16 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
         {
             const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3),
                            dn = digits4(wn);
-            uint4* vq = reinterpret_cast<uint4*>(V + lp0);
-            vq[0] = vquad(d0, d1);
-            vq[1] = vquad(d1, d2);
-            vq[2] = vquad(d2, d3);
-            vq[3] = vquad(d3, dn);
+            char* const vb = reinterpret_cast<char*>(V);
+            const uint32_t vo = 4u * static_cast<uint32_t>(lp0);
+            *reinterpret_cast<uint4*>(vb + v_swz(vo)) = vquad(d0, d1);
+            *reinterpret_cast<uint4*>(vb + v_swz(vo + 16)) = vquad(d1, d2);
+            *reinterpret_cast<uint4*>(vb + v_swz(vo + 32)) = vquad(d2, d3);
+            *reinterpret_cast<uint4*>(vb + v_swz(vo + 48)) = vquad(d3, dn);
             if (tid == 0) {  // halo positions -8..-1 (local 8..15)
                 const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
-                uint4* hq = reinterpret_cast<uint4*>(V + 8);
-                hq[0] = vquad(dp2, dp3);
-                hq[1] = vquad(dp3, d0);
+                *reinterpret_cast<uint4*>(vb + v_swz(32)) = vquad(dp2, dp3);
+                *reinterpret_cast<uint4*>(vb + v_swz(48)) = vquad(dp3, d0);
             }
         }
         {
@@ -462,13 +490,14 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             lane_excl[p] = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) val[p][k] = 0;
-            if (kPWorkerThreads * 8 * p >= n_tile) continue;  // block-uniform
+            if (8u * (kPWorkerThreads * p + 32 * warp) >= n_tile) continue;  // warp-uniform: no ints here
             if (8 * u < n_tile) {
                 const uint4 qa = *reinterpret_cast<const uint4*>(EPw + 4 + 8 * u);
                 const uint4 qb = *reinterpret_cast<const uint4*>(EPw + 8 + 8 * u);
                 const uint32_t xs[9] = {EPw[3 + 8 * u], qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
-                for (int k = 0; k < 8; ++k) val[p][k] = lds_at(V, xs[k] >> 16) & bmsk((xs[k + 1] - xs[k]) & 0xFFFFu);
+                for (int k = 0; k < 8; ++k)
+                    val[p][k] = lds_at(V, v_swz(xs[k] >> 16)) & bmsk((xs[k + 1] - xs[k]) & 0xFFFFu);
             }
             if (kDelta) {
 #pragma unroll
@@ -487,7 +516,8 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
         if (kDelta) {
             workers_sync();  // bar #3: pass sums
             const uint32_t x =
-                (lane < kPasses * kPWorkers && kPWorkerThreads * 8 * (lane / kPWorkers) < n_tile) ? s_pass_sum[lane] : 0u;
+                (lane < kPasses * kPWorkers && 8u * (kPWorkerThreads * (lane / kPWorkers) + 32 * (lane % kPWorkers)) < n_tile)
+                    ? s_pass_sum[lane] : 0u;
             uint32_t sc = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -505,15 +535,14 @@ __global__ void __launch_bounds__(kPThreads, 3) vbyte_decode_pipelined(Params P)
             }
         }
         // park the values (delta: in-tile inclusive prefix) until the lookback resolves t_i
-        uint32_t* vals = VAL[cb];
+        uint4* vals = reinterpret_cast<uint4*>(VAL[cb]);
 #pragma unroll
         for (int p = 0; p < kPasses; ++p) {
-            if (kPWorkerThreads * 8 * p >= n_tile) continue;
+            if (8u * (kPWorkerThreads * p + 32 * warp) >= n_tile) continue;
             const unsigned u = tid + kPWorkerThreads * p;
             const uint32_t e = lane_excl[p];
-            uint4* dst = reinterpret_cast<uint4*>(vals + 8 * u);
-            dst[0] = make_uint4(val[p][0] + e, val[p][1] + e, val[p][2] + e, val[p][3] + e);
-            dst[1] = make_uint4(val[p][4] + e, val[p][5] + e, val[p][6] + e, val[p][7] + e);
+            vals[val_chunk(2 * u)] = make_uint4(val[p][0] + e, val[p][1] + e, val[p][2] + e, val[p][3] + e);
+            vals[val_chunk(2 * u + 1)] = make_uint4(val[p][4] + e, val[p][5] + e, val[p][6] + e, val[p][7] + e);
         }
     }
 

@@ -133,7 +133,7 @@ __device__ unsigned long long lb3_resolve(LB3& L, const unsigned long long* d0, 
                                           int lane) {
     long long base2 = ((t >> 5) >> 5) - 1;
     unsigned long long acc = 0;
-    unsigned backoff = 64;
+    unsigned backoff = 32;
     while (true) {
         bool adv;
         unsigned long long part = 0;
@@ -151,8 +151,8 @@ __device__ unsigned long long lb3_resolve(LB3& L, const unsigned long long* d0, 
             // by pretending the tile and group are first in their parents
             t = (t >> 10) << 10;
         } else {
-            __nanosleep(backoff);
-            backoff = backoff < 1024 ? backoff * 2 : 1024;
+            __nanosleep(backoff);  // short cap: a sleeping poller adds its sleep to the chain
+            backoff = backoff < 256 ? backoff * 2 : 256;
         }
         lb3_poll<kWide>(L, d0, d1, d2, t, base2, epoch, lane);
     }

@@ -15,6 +15,7 @@
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
 #include "decode_pipelined.cuh"
+#include "decode_v3.cuh"
 #include "decode_warp.cuh"
 #include "totals_kernel.cuh"
 
@@ -51,7 +52,8 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
-// Strict-mode kernel: 0 CTA-pipelined (default), 1 per-tile kernel, 2 warp-tile kernel.
+// Strict-mode kernel: 0 CTA-pipelined (default), 1 per-tile kernel, 2 warp-tile kernel,
+// 3 warp-sliced v3 (decode_v3.cuh; fastest on all-1-byte data, otherwise slower).
 // Permissive mode always runs the per-tile kernel (it needs a third lookback
 // component inside phase 1).  The switch exists for profiling comparisons.
 int g_kernel_choice = 0;
@@ -87,6 +89,32 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
     const long long cap = static_cast<long long>(per_sm) * sms;
     const unsigned grid = static_cast<unsigned>(p.n_tiles < cap ? p.n_tiles : cap);
     mvbk::vbyte_decode_pipelined<Delta, Trace><<<grid, mvbk::kPThreads, mvbk::kSmemBytes, s>>>(p);
+    return cudaGetLastError();
+}
+
+// Persistent warp-sliced launch (default strict kernel, decode_v3.cuh).
+template <bool Delta>
+cudaError_t launch_v3(const mvbk::WParams& p, cudaStream_t s) {
+    static int per_sm = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 0) {
+        e = cudaFuncSetAttribute(mvbk::vbyte_decode_v3<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kS3Bytes);
+        if (e != cudaSuccess) return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_v3<Delta>, mvbk::kV3Threads,
+                                                          mvbk::kS3Bytes);
+        if (e != cudaSuccess) return e;
+        per_sm = n > 0 ? n : 1;
+    }
+    const long long cap = static_cast<long long>(per_sm) * sms;
+    const unsigned grid = static_cast<unsigned>(p.p.n_tiles < cap ? p.p.n_tiles : cap);
+    mvbk::vbyte_decode_v3<Delta><<<grid, mvbk::kV3Threads, mvbk::kS3Bytes, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -141,8 +169,10 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     const size_t scan = scan_length(in_len, count);
     const size_t tiles = tiles_for(mis, scan);
     const bool warp_kernel = mode == MVB_STRICT && g_kernel_choice == 2 && trace == nullptr;
+    const bool v3_kernel = mode == MVB_STRICT && g_kernel_choice == 3;
     const size_t wtiles = wtiles_for(mis, scan);
-    if (ws == nullptr || ws_bytes < (warp_kernel ? ws_need_warp(wtiles) : ws_need(tiles))) return MVB_ERR_WORKSPACE;
+    const size_t need = warp_kernel ? ws_need_warp(wtiles) : v3_kernel ? ws_need_warp(tiles) : ws_need(tiles);
+    if (ws == nullptr || ws_bytes < need) return MVB_ERR_WORKSPACE;
     if (wtiles >= (1ull << 40)) return MVB_ERR_INVALID_ARG;
 
     Params p;
@@ -167,7 +197,25 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.trace = trace;
 
     cudaError_t e;
-    if (warp_kernel) {
+    if (v3_kernel) {
+        // three-level descriptor layout of decode_warp.cuh, over 4 KiB tiles
+        mvbk::WParams w;
+        w.p = p;
+        const size_t ng = (tiles + 31) / 32, ns = (ng + 31) / 32;
+        w.n_groups = static_cast<long long>(ng);
+        w.n_super = static_cast<long long>(ns);
+        w.p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
+        w.p.dsum = w.p.dcnt + tiles;
+        w.g1cnt = w.p.dsum + tiles;
+        w.g1sum = w.g1cnt + ng;
+        w.g2cnt = w.g1sum + ng;
+        w.g2sum = w.g2cnt + ns;
+        w.a1cnt = w.g2sum + ns;
+        w.a1sum = w.a1cnt + ng;
+        w.a2cnt = w.a1sum + ng;
+        w.a2sum = w.a2cnt + ns;
+        e = delta ? launch_v3<true>(w, stream) : launch_v3<false>(w, stream);
+    } else if (warp_kernel) {
         mvbk::WParams w;
         w.p = p;
         w.p.n_tiles = static_cast<unsigned>(wtiles);

@@ -21,6 +21,8 @@ tag = ("_" + sys.argv[2]) if len(sys.argv) > 2 else ""
 w = {"c1": W.config1, "c2": W.config2, "all1": lambda: W.config5("all1"), "all5": lambda: W.config5("all5")}[cfg]()
 dev = torch.device("cuda", 0)
 L = _lib.lib()
+if os.environ.get("MVB_KERNEL"):  # strict kernel variant to trace (3 = warp-sliced v3)
+    _lib.set_kernel_choice(int(os.environ["MVB_KERNEL"]))
 L.mvbx_decode_traced.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32,
                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                  ctypes.c_void_p, ctypes.c_void_p]

@@ -283,9 +283,9 @@ def test_config4_full_size_device(golden, oracle, cuda):
     assert oracle.fnv_u32(got) == s["out_fnv"]
 
 
-@pytest.mark.parametrize("choice", [1, 2, 0])
+@pytest.mark.parametrize("choice", [1, 2, 3, 0])
 def test_every_strict_kernel_variant(choice, golden, oracle):
-    """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined) agree with
+    """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined, warp-sliced) agree with
     the oracle on KATs, errors across tile boundaries and a full config."""
     from paper_1503_07387_b200 import _lib
 
