@@ -11,11 +11,13 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
 #include "decode_pipelined.cuh"
 #include "decode_v3.cuh"
+#include "decode_seg.cuh"
 #include "decode_warp.cuh"
 #include "totals_kernel.cuh"
 
@@ -47,6 +49,26 @@ size_t ws_need_warp(size_t wtiles) {
 
 // Bytes the decode of `count` integers can touch: every integer (strict or
 // permissive) spans at most 5 bytes, so nothing past 5*count matters.
+// Workspace layout tracking.  Every kernel family keeps its group
+// accumulators zero between launches (its finalizing CTA re-zeroes them), but
+// the accumulators' offset depends on the family and the launch size, so a
+// launch with a different layout than the previous one on the same workspace
+// could find stale descriptor words where it expects zeros.  The host
+// remembers each workspace's last layout and re-zeroes the used region when
+// it changes (steady-state repeated launches never pay for it).
+std::mutex g_ws_mu;
+std::unordered_map<const void*, unsigned long long> g_ws_layout;
+
+cudaError_t prepare_workspace(void* ws, size_t used_bytes, unsigned long long layout, cudaStream_t s) {
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        auto it = g_ws_layout.find(ws);
+        if (it != g_ws_layout.end() && it->second == layout) return cudaSuccess;
+        g_ws_layout[ws] = layout;
+    }
+    return cudaMemsetAsync(static_cast<char*>(ws) + kHeaderBytes, 0, used_bytes - kHeaderBytes, s);
+}
+
 size_t scan_length(size_t in_len, size_t count) {
     if (count > in_len / 5 + 1) return in_len;
     return std::min(in_len, count * 5);
@@ -92,7 +114,65 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// Persistent warp-sliced launch (default strict kernel, decode_v3.cuh).
+// Two-kernel segmented strict decode (decode_seg.cuh): group accumulators
+// zeroed, segment totals, then one warp per segment.
+template <bool Delta>
+int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+    static int per_sm = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return MVB_ERR_CUDA;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return MVB_ERR_CUDA;
+    if (per_sm < 0) {
+        if (cudaFuncSetAttribute(mvbk::vbyte_seg_decode<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kSegSmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_decode<Delta>, mvbk::kSegThreads,
+                                                          mvbk::kSegSmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        per_sm = n > 0 ? n : 1;
+    }
+    const long long ctas = static_cast<long long>(per_sm) * sms;
+    const long long warps = ctas * mvbk::kSegWarps;
+    const long long qlen = p.mis + p.len;
+    long long seg = (qlen + 4 * warps - 1) / (4 * warps);
+    seg = (seg + mvbk::kSegSlice - 1) / mvbk::kSegSlice * mvbk::kSegSlice;
+    if (seg < mvbk::kSegSlice) seg = mvbk::kSegSlice;
+    const long long n_seg = (qlen + seg - 1) / seg;
+    const long long n_grp = (n_seg + 31) / 32;
+    const size_t need = kHeaderBytes + 8 * static_cast<size_t>(n_seg) + 16 * static_cast<size_t>(n_grp);
+    if (ws_bytes < need) return MVB_ERR_WORKSPACE;
+    mvbk::SegParams S;
+    S.in = p.in;
+    S.mis = p.mis;
+    S.len = p.len;
+    S.count = p.count;
+    S.out = p.out;
+    S.prev = p.prev;
+    S.prev_dev = p.prev_dev;
+    S.seg_bytes = seg;
+    S.n_seg = n_seg;
+    S.n_grp = n_grp;
+    char* b = static_cast<char*>(ws) + kHeaderBytes;
+    S.gcnt = reinterpret_cast<unsigned long long*>(b);
+    S.gsum = S.gcnt + n_grp;
+    S.scnt = reinterpret_cast<unsigned*>(S.gsum + n_grp);
+    S.ssum = S.scnt + n_seg;
+    S.hdr = p.hdr;
+    S.res_dev = p.res_dev;
+    if (prepare_workspace(ws, need, (4ull << 56) | static_cast<unsigned long long>(n_seg), s) != cudaSuccess)
+        return MVB_ERR_CUDA;
+    const long long ga = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
+    const unsigned grid_a = static_cast<unsigned>(ga < ctas * 2 ? ga : ctas * 2);
+    mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, 0, s>>>(S);
+    const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
+    const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
+    mvbk::vbyte_seg_decode<Delta><<<grid_b, mvbk::kSegThreads, mvbk::kSegSmem, s>>>(S);
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+// Persistent warp-sliced launch (decode_v3.cuh).
 template <bool Delta>
 cudaError_t launch_v3(const mvbk::WParams& p, cudaStream_t s) {
     static int per_sm = -1;
@@ -196,6 +276,13 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.res_dev = res_dev;
     p.trace = trace;
 
+    if (mode == MVB_STRICT && g_kernel_choice == 4 && trace == nullptr)
+        return delta ? launch_seg<true>(p, ws, ws_bytes, stream) : launch_seg<false>(p, ws, ws_bytes, stream);
+    {
+        const unsigned long long family = warp_kernel ? 2 : v3_kernel ? 3 : 1;
+        const unsigned long long units = warp_kernel ? wtiles : tiles;
+        if (prepare_workspace(ws, need, (family << 56) | units, stream) != cudaSuccess) return MVB_ERR_CUDA;
+    }
     cudaError_t e;
     if (v3_kernel) {
         // three-level descriptor layout of decode_warp.cuh, over 4 KiB tiles
@@ -320,6 +407,10 @@ size_t mvb_workspace_bytes(size_t in_len) {
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
     if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        g_ws_layout.erase(ws);
+    }
     return cudaMemsetAsync(ws, 0, ws_bytes, stream) == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 

@@ -283,7 +283,7 @@ def test_config4_full_size_device(golden, oracle, cuda):
     assert oracle.fnv_u32(got) == s["out_fnv"]
 
 
-@pytest.mark.parametrize("choice", [1, 2, 3, 0])
+@pytest.mark.parametrize("choice", [1, 2, 3, 4, 0])
 def test_every_strict_kernel_variant(choice, golden, oracle):
     """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined, warp-sliced) agree with
     the oracle on KATs, errors across tile boundaries and a full config."""
@@ -320,5 +320,34 @@ def test_every_strict_kernel_variant(choice, golden, oracle):
         r, out = gpu_decode(w.encoded, w.count, delta=True)
         assert r == (s["status"], s["values_written"], s["bytes_consumed"])
         assert oracle.fnv_u32(out) == s["out_fnv"]
+    finally:
+        _lib.set_kernel_choice(0)
+
+
+def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
+    """One Decoder (one workspace) serving decodes of different sizes, both
+    modes and every strict kernel: accumulators left by one launch layout must
+    never leak into another (they live at size-dependent offsets)."""
+    import torch
+
+    from paper_1503_07387_b200 import _lib
+
+    d = mvb.Decoder(cuda, 1 << 20)
+    streams = []
+    for n, seed in ((300000, 1), (700, 2), (60000, 3), (5, 4), (150000, 5)):
+        v = W.mixed_values(n, seed)
+        streams.append((v, oracle.encode_sequence(v)))
+    try:
+        for choice in (0, 4, 1, 3, 2, 0):
+            _lib.set_kernel_choice(choice)
+            for rep in range(2):
+                for (v, enc), mode in zip(streams * 2, [STRICT] * 5 + [PERMISSIVE] * 5):
+                    src = torch.from_numpy(enc).to(cuda)
+                    out = torch.empty(v.size, dtype=torch.int32, device=cuda)
+                    d.decode_delta(src, v.size, 9, out, mode)
+                    r = d.result()
+                    ro, oo = oracle.decode_delta(enc, v.size, 9, mode)
+                    assert (int(r.status), r.values_written, r.bytes_consumed) == tuple(ro), (choice, v.size, mode)
+                    assert np.array_equal(out.cpu().numpy().view(np.uint32), oo), (choice, v.size, mode)
     finally:
         _lib.set_kernel_choice(0)
