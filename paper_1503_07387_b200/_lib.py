@@ -100,8 +100,8 @@ def lib():
 
 def set_kernel_choice(choice: int) -> None:
     """Profiling/testing switch (internal symbol mvbx_set_kernel): strict-mode
-    kernel 0 = CTA-pipelined (default), 1 = per-tile, 2 = warp-tile,
-    3 = warp-sliced v3."""
+    kernel 0 = segmented two-kernel (default), 1 = per-tile, 2 = warp-tile,
+    3 = warp-sliced v3, 4 = CTA-pipelined single pass."""
     f = lib().mvbx_set_kernel
     f.argtypes = [ctypes.c_int]
     f.restype = None

@@ -89,78 +89,172 @@ __device__ __forceinline__ uint32_t seg_inr16(const SegParams& S, long long q0) 
 
 // ------------------------------------------------------------------ kernel A
 
+// Digit-weight sum of one word w (bytes b0..b3) given the 8 preceding bytes
+// (p1 = the word before w, p2 = the one before that): every byte's digit
+// times 128^(its position within its integer), mod 2^32.  The position is
+// read off the high bits of the 1..5 preceding bytes in byte lanes (SWAR):
+// position 0 after a terminator, 1 after one continuation byte, ...
+// Classes 0/1 weigh 1/128 in one dp4a, 2/3 weigh 2^14/2^21 in a second, 4
+// weighs 2^28 in a third (only when `hi`: some byte follows >= 2
+// continuation bytes).  `keep` (0x80 per byte) selects the bytes counted.
+__device__ __forceinline__ uint32_t word_digit_sum(uint32_t w, uint32_t p1, uint32_t p2, uint32_t keep, bool hi) {
+    const uint32_t c1 = __funnelshift_l(p1, w, 8) & 0x80808080u;   // byte before is a continuation byte
+    const uint32_t c2 = __funnelshift_l(p1, w, 16) & 0x80808080u;  // 2 before
+    const uint32_t b = w & 0x7F7F7F7Fu;
+    const uint32_t k0 = ~c1 & keep, k1 = c1 & ~c2 & keep;
+    uint32_t s = __dp4a(b, ((k0 >> 7) & 0x01010101u) | (k1 & 0x80808080u), 0u);
+    if (hi) {
+        const uint32_t c3 = __funnelshift_l(p1, w, 24) & 0x80808080u;
+        const uint32_t c4 = p1 & 0x80808080u;
+        const uint32_t c5 = __funnelshift_l(p2, p1, 8) & 0x80808080u;
+        const uint32_t cc = c1 & c2 & keep;
+        const uint32_t k2 = cc & ~c3, k3 = cc & c3 & ~c4, k4 = cc & c3 & c4 & ~c5;
+        s += __dp4a(b, ((k2 >> 7) & 0x01010101u) | (k3 & 0x80808080u), 0u) << 14;
+        s += __dp4a(b, (k4 >> 7) & 0x01010101u, 0u) << 28;
+    }
+    return s;
+}
+
+// Bytes of word w that follow its last terminator byte (0x80 per byte);
+// all four if w has none.
+__device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
+    const uint32_t t = ~w & 0x80808080u;
+    if (!t) return 0x80808080u;
+    const int hb = 31 - __clz(t);  // bit 7 + 8*i of the last terminator byte i
+    return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
+}
+
+constexpr int kSegASlice = 2048;  // kernel A: 64 contiguous bytes (4 chunks) per lane per iteration
+
+// One warp walks a contiguous run of segments in 2 KiB iterations (lane l:
+// bytes 64l..64l+63), prefetching the next iteration across segment
+// boundaries.  An integer belongs to the segment holding its terminator: the
+// digit sum adds the bytes before a segment that belong to its first integer
+// (head, at most 4: lane 0's halo word) and leaves out the bytes after its
+// last terminator (tail, at most 4 in canonical data: lane 31's last words).
 template <bool kDelta>
 __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    for (long long s = gw; s < S.n_seg; s += nw) {
-        const long long qs = s * S.seg_bytes;
-        const long long qe = qs + S.seg_bytes;
-        // previous 8 bytes of the first slice (lane 0)
-        uint32_t pw2 = 0, pw3 = 0;
-        if (lane == 0) {
-            if (seg_inside(S, qs - 8, 8)) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(S.in - S.mis + qs - 8));
-                pw2 = v.x;
-                pw3 = v.y;
-            } else {
-                pw2 = seg_word(S, qs - 8);
-                pw3 = seg_word(S, qs - 4);
-            }
+    const long long per = (S.n_seg + nw - 1) / nw;
+    const long long s_begin = gw * per;
+    const long long s_end = s_begin + per < S.n_seg ? s_begin + per : S.n_seg;
+    if (s_begin >= s_end) return;
+    const long long its_per_seg = S.seg_bytes / kSegASlice;
+    const long long q_begin = s_begin * S.seg_bytes, q_end = s_end * S.seg_bytes;
+
+    uint32_t pw2 = 0, pw3 = 0;  // the 8 bytes before the current iteration (for lane 0)
+    if (lane == 0) {
+        if (seg_inside(S, q_begin - 8, 8)) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(S.in - S.mis + q_begin - 8));
+            pw2 = v.x;
+            pw3 = v.y;
+        } else {
+            pw2 = seg_word(S, q_begin - 8);
+            pw3 = seg_word(S, q_begin - 4);
         }
-        unsigned cnt = 0;
-        uint32_t sum = 0;
-        for (long long q = qs; q < qe; q += kSegSlice) {
-            const long long q0 = q + 16 * lane;
-            const uint4 x = seg_load16(S, q0);
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-            uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, x.z, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, x.w, 1);
-            uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, x.x, 1);
-            const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, x.z, 31), l3 = __shfl_sync(0xFFFFFFFFu, x.w, 31);
-            if (lane == 0) {
-                wp2 = pw2;
-                wp3 = pw3;
-            }
-            if (lane == 31) wn = seg_inside(S, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(S.in - S.mis + q0 + 16))
-                                                           : seg_word(S, q0 + 16);
-            pw2 = l2;
-            pw3 = l3;
-            const uint32_t T16 = hibits16(~w[0], ~w[1], ~w[2], ~w[3]);
-            const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
-            uint32_t ends = T16 & seg_inr16(S, q0);
-            cnt += __popc(ends);
-            if (kDelta) {
-                const uint32_t single = ends & (Tx >> 7);
+    }
+    uint4 nx[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t m = (single >> (4 * k)) & 0xFu;
-                    sum = __dp4a(w[k] & (((m * 0x204081u) & 0x01010101u) * 0xFFu), 0x01010101u, sum);
-                }
-                ends &= ~single;
-                if (ends) {
-                    const uint32_t d[6] = {digits4(wp2), digits4(wp3), digits4(w[0]), digits4(w[1]), digits4(w[2]),
-                                           digits4(w[3])};
-                    while (ends) {
-                        const int j = __ffs(ends) - 1;
-                        ends &= ends - 1;
-                        sum += value_ending_at(j, Tx, d);
-                    }
-                }
+    for (int c = 0; c < 4; ++c) nx[c] = seg_load16(S, q_begin + 64 * lane + 16 * c);
+    unsigned cnt = 0;
+    uint32_t sum = 0;
+    long long s = s_begin;
+    long long it = 0;  // iteration within segment s
+    for (long long q = q_begin; q < q_end; q += kSegASlice) {
+        uint32_t w[18];  // w[0], w[1]: the 8 bytes before this lane's 64; w[2..17]: its 64 bytes
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            w[2 + 4 * c] = nx[c].x;
+            w[3 + 4 * c] = nx[c].y;
+            w[4 + 4 * c] = nx[c].z;
+            w[5 + 4 * c] = nx[c].w;
+        }
+        if (q + kSegASlice < q_end) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) nx[c] = seg_load16(S, q + kSegASlice + 64 * lane + 16 * c);
+        }
+        w[0] = __shfl_up_sync(0xFFFFFFFFu, w[16], 1);
+        w[1] = __shfl_up_sync(0xFFFFFFFFu, w[17], 1);
+        const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w[16], 31), l3 = __shfl_sync(0xFFFFFFFFu, w[17], 31);
+        if (lane == 0) {
+            w[0] = pw2;
+            w[1] = pw3;
+        }
+        pw2 = l2;
+        pw3 = l3;
+        const bool seg_first = it == 0, seg_last = it == its_per_seg - 1;
+        const long long ql = q + 64 * lane;
+        const bool edge = !seg_inside(S, ql, 64);  // stream start / end inside these 64 bytes
+        uint32_t C[18];  // continuation flags (0x80 per byte)
+#pragma unroll
+        for (int k = 0; k < 18; ++k) C[k] = w[k] & 0x80808080u;
+        if (!edge) {
+            unsigned nc = 0;
+#pragma unroll
+            for (int k = 2; k < 18; ++k) nc += __popc(C[k]);
+            cnt += 64 - nc;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t T16 = hibits16(~w[2 + 4 * c], ~w[3 + 4 * c], ~w[4 + 4 * c], ~w[5 + 4 * c]);
+                cnt += __popc(T16 & seg_inr16(S, ql + 16 * c));
             }
         }
-        cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
         if (kDelta) {
+            // classes 0/1 for all 16 words (weights 1 / 128 per byte, one dp4a each)
+            uint32_t hiacc = 0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-        }
-        if (lane == 0) {
-            S.scnt[s] = cnt;
-            atomicAdd(S.gcnt + (s >> 5), static_cast<unsigned long long>(cnt));
-            if (kDelta) {
-                S.ssum[s] = sum;
-                atomicAdd(S.gsum + (s >> 5), static_cast<unsigned long long>(sum));
+            for (int k = 2; k < 18; ++k) {
+                const uint32_t c1 = __funnelshift_l(C[k - 1], C[k], 8), c2 = __funnelshift_l(C[k - 1], C[k], 16);
+                hiacc |= c1 & c2;
+                sum = __dp4a(w[k] & 0x7F7F7F7Fu, ((c1 >> 7) ^ 0x01010101u) | (c1 & ~c2), sum);
             }
+            if (__any_sync(0xFFFFFFFFu, hiacc)) {
+                // integers of 3..5 bytes somewhere in the warp: classes 2..4
+#pragma unroll
+                for (int k = 2; k < 18; ++k) {
+                    const uint32_t c1 = __funnelshift_l(C[k - 1], C[k], 8), c2 = __funnelshift_l(C[k - 1], C[k], 16);
+                    const uint32_t c3 = __funnelshift_l(C[k - 1], C[k], 24), c4 = C[k - 1];
+                    const uint32_t c5 = __funnelshift_l(C[k - 2], C[k - 1], 8);
+                    const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
+                    sum += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3 & ~c4), 0u) << 14;
+                    sum += __dp4a(b, (cc & c3 & c4 & ~c5) >> 7, 0u) << 28;
+                }
+            }
+            if (seg_first && lane == 0) {
+                // head: bytes -4..-1 of the first integer ending in the segment
+                sum += word_digit_sum(w[1], w[0], 0u, after_last_terminator(w[1]), true);
+            }
+            if (seg_last && lane == 31) {
+                // tail: bytes after the segment's last terminator (in the last two words)
+                const uint32_t a17 = after_last_terminator(w[17]);
+                const uint32_t a16 = (~w[17] & 0x80808080u) ? 0u : after_last_terminator(w[16]);
+                sum -= word_digit_sum(w[17], w[16], w[15], a17, true) + word_digit_sum(w[16], w[15], w[14], a16, true);
+            }
+        }
+        if (seg_last) {
+            const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
+            uint32_t s_tot = sum;
+            if (kDelta) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s_tot += __shfl_xor_sync(0xFFFFFFFFu, s_tot, o);
+            }
+            if (lane == 0) {
+                S.scnt[s] = c_tot;
+                atomicAdd(S.gcnt + (s >> 5), static_cast<unsigned long long>(c_tot));
+                if (kDelta) {
+                    S.ssum[s] = s_tot;
+                    atomicAdd(S.gsum + (s >> 5), static_cast<unsigned long long>(s_tot));
+                }
+            }
+            cnt = 0;
+            sum = 0;
+            ++s;
+            it = 0;
+        } else {
+            ++it;
         }
     }
 }

@@ -74,8 +74,9 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
-// Strict-mode kernel: 0 CTA-pipelined (default), 1 per-tile kernel, 2 warp-tile kernel,
-// 3 warp-sliced v3 (decode_v3.cuh; fastest on all-1-byte data, otherwise slower).
+// Strict-mode kernel: 0 segmented two-kernel decode (default, decode_seg.cuh), 1 per-tile
+// kernel, 2 warp-tile kernel, 3 warp-sliced v3 (decode_v3.cuh), 4 CTA-pipelined single pass
+// (decode_pipelined.cuh; also the traced kernel).
 // Permissive mode always runs the per-tile kernel (it needs a third lookback
 // component inside phase 1).  The switch exists for profiling comparisons.
 int g_kernel_choice = 0;
@@ -137,8 +138,8 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     const long long warps = ctas * mvbk::kSegWarps;
     const long long qlen = p.mis + p.len;
     long long seg = (qlen + 4 * warps - 1) / (4 * warps);
-    seg = (seg + mvbk::kSegSlice - 1) / mvbk::kSegSlice * mvbk::kSegSlice;
-    if (seg < mvbk::kSegSlice) seg = mvbk::kSegSlice;
+    seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: 2 KiB slices
+    if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
     const long long n_seg = (qlen + seg - 1) / seg;
     const long long n_grp = (n_seg + 31) / 32;
     const size_t need = kHeaderBytes + 8 * static_cast<size_t>(n_seg) + 16 * static_cast<size_t>(n_grp);
@@ -163,8 +164,17 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     S.res_dev = p.res_dev;
     if (prepare_workspace(ws, need, (4ull << 56) | static_cast<unsigned long long>(n_seg), s) != cudaSuccess)
         return MVB_ERR_CUDA;
-    const long long ga = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
-    const unsigned grid_a = static_cast<unsigned>(ga < ctas * 2 ? ga : ctas * 2);
+    static int per_sm_a = -1;
+    if (per_sm_a < 0) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads, 0) !=
+            cudaSuccess)
+            return MVB_ERR_CUDA;
+        per_sm_a = n > 0 ? n : 1;
+    }
+    const long long ga = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;  // at least one segment per warp
+    const long long cap_a = static_cast<long long>(per_sm_a) * sms;
+    const unsigned grid_a = static_cast<unsigned>(ga < cap_a ? ga : cap_a);
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, 0, s>>>(S);
     const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
     const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
@@ -276,7 +286,7 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.res_dev = res_dev;
     p.trace = trace;
 
-    if (mode == MVB_STRICT && g_kernel_choice == 4 && trace == nullptr)
+    if (mode == MVB_STRICT && g_kernel_choice == 0 && trace == nullptr)
         return delta ? launch_seg<true>(p, ws, ws_bytes, stream) : launch_seg<false>(p, ws, ws_bytes, stream);
     {
         const unsigned long long family = warp_kernel ? 2 : v3_kernel ? 3 : 1;
@@ -321,7 +331,7 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
         w.a2sum = w.a2cnt + ns;
         e = delta ? launch_warp<true>(w, static_cast<unsigned>(wtiles), stream)
                   : launch_warp<false>(w, static_cast<unsigned>(wtiles), stream);
-    } else if (mode == MVB_STRICT && (g_kernel_choice == 0 || trace != nullptr))
+    } else if (mode == MVB_STRICT && (g_kernel_choice == 4 || g_kernel_choice == 0 || trace != nullptr))
         e = delta ? launch_pipelined<true>(p, stream) : launch_pipelined<false>(p, stream);
     else if (delta)
         e = mode == MVB_STRICT ? launch<true, mvbk::MODE_STRICT>(p, stream)

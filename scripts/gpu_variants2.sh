@@ -11,7 +11,7 @@ for name, w in cfgs.items():
     src = torch.from_numpy(w.encoded).to(dev); out = torch.empty(w.count, dtype=torch.int32, device=dev)
     d = mvb.Decoder(dev, w.encoded.size); exp = torch.from_numpy(w.expected().view(np.int32)).to(dev)
     row = []
-    for ch in (0, 4, 3):
+    for ch in (0, 4):
         _lib.set_kernel_choice(ch)
         ts = []
         for it in range(12):

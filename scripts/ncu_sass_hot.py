@@ -16,8 +16,8 @@ ix = {k: i for i, k in enumerate(hdr)}
 body = [r for r in rows[2:] if len(r) == len(hdr)]
 tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in body)
 inst = sum(int(r[ix["Instructions Executed"]] or 0) for r in body)
-wf = sum(int(r[ix["L1 Wavefronts Shared"]] or 0) for r in body)
-wfi = sum(int(r[ix["L1 Wavefronts Shared Ideal"]] or 0) for r in body)
+wf = sum(int(r[ix["L1 Wavefronts Shared"]] or 0) for r in body) if "L1 Wavefronts Shared" in ix else 0
+wfi = sum(int(r[ix["L1 Wavefronts Shared Ideal"]] or 0) for r in body) if "L1 Wavefronts Shared Ideal" in ix else 0
 print(f"samples {tot}  instructions {inst}  smem wavefronts {wf} (ideal {wfi})")
 order = sorted(range(len(body)), key=lambda i: -int(body[i][ix["Warp Stall Sampling (All Samples)"]] or 0))
 for i in order[:n]:
