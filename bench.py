@@ -359,7 +359,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": 4 * count + ctypes.sizeof(_lib.MvbResult),
                     "api": "mvb_decode_delta_stream (host pointers, pinned)" if w.delta else
                            "mvb_decode_stream (host pointers, pinned)"},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * _lib.kernels_per_decode(0),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

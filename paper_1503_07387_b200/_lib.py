@@ -98,6 +98,14 @@ def lib():
     return _lib
 
 
+def kernels_per_decode(mode: int = 0) -> int:
+    """Kernels one decode call launches in steady state (internal symbol)."""
+    f = lib().mvbx_kernels_per_decode
+    f.argtypes = [ctypes.c_int]
+    f.restype = ctypes.c_int
+    return int(f(int(mode)))
+
+
 def set_kernel_choice(choice: int) -> None:
     """Profiling/testing switch (internal symbol mvbx_set_kernel): strict-mode
     kernel 0 = segmented two-kernel (default), 1 = per-tile, 2 = warp-tile,

@@ -530,6 +530,10 @@ int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
+// Kernels one decode call launches in steady state (bench accounting; the
+// workspace re-zeroing memset runs only when a workspace changes layout).
+int mvbx_kernels_per_decode(int mode) { return (mode == MVB_STRICT && g_kernel_choice == 0) ? 2 : 1; }
+
 const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }
 
 }  // extern "C"

@@ -281,8 +281,8 @@ class DeviceShard:
         self.carry = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.dec = mvb.Decoder(self.device, capacity_bytes=max(self.bound, 1))
         self.gather = gather
-        self.launches_per_pass = 1 + (2 if delta and world > 1 and rank < world - 1 else
-                                      1 if delta and world > 1 else 0)
+        self.launches_per_pass = _lib.kernels_per_decode(0) + (2 if delta and world > 1 and rank < world - 1 else
+                                                             1 if delta and world > 1 else 0)
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
