@@ -124,10 +124,12 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
     return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
 }
 
-constexpr int kSegASlice = 2048;  // kernel A: 64 contiguous bytes (4 chunks) per lane per iteration
+constexpr int kSegAChunks = 2;                     // kernel A: 16-byte chunks per lane per iteration
+constexpr int kSegASlice = 512 * kSegAChunks;      // bytes per warp iteration
+constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + the lane's bytes
 
-// One warp walks a contiguous run of segments in 2 KiB iterations (lane l:
-// bytes 64l..64l+63), prefetching the next iteration across segment
+// One warp walks a contiguous run of segments in kSegASlice-byte iterations
+// (lane l: 16*kSegAChunks contiguous bytes), prefetching the next iteration across segment
 // boundaries.  An integer belongs to the segment holding its terminator: the
 // digit sum adds the bytes before a segment that belong to its first integer
 // (head, at most 4: lane 0's halo word) and leaves out the bytes after its
@@ -155,17 +157,18 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
             pw3 = seg_word(S, q_begin - 4);
         }
     }
-    uint4 nx[4];
+    constexpr int L = 16 * kSegAChunks;  // bytes per lane per iteration
+    uint4 nx[kSegAChunks];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) nx[c] = seg_load16(S, q_begin + 64 * lane + 16 * c);
+    for (int c = 0; c < kSegAChunks; ++c) nx[c] = seg_load16(S, q_begin + L * lane + 16 * c);
     unsigned cnt = 0;
     uint32_t sum = 0;
     long long s = s_begin;
     long long it = 0;  // iteration within segment s
     for (long long q = q_begin; q < q_end; q += kSegASlice) {
-        uint32_t w[18];  // w[0], w[1]: the 8 bytes before this lane's 64; w[2..17]: its 64 bytes
+        uint32_t w[kSegAW];  // w[0], w[1]: the 8 bytes before this lane's bytes; then the lane's words
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < kSegAChunks; ++c) {
             w[2 + 4 * c] = nx[c].x;
             w[3 + 4 * c] = nx[c].y;
             w[4 + 4 * c] = nx[c].z;
@@ -173,11 +176,11 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
         }
         if (q + kSegASlice < q_end) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) nx[c] = seg_load16(S, q + kSegASlice + 64 * lane + 16 * c);
+            for (int c = 0; c < kSegAChunks; ++c) nx[c] = seg_load16(S, q + kSegASlice + L * lane + 16 * c);
         }
-        w[0] = __shfl_up_sync(0xFFFFFFFFu, w[16], 1);
-        w[1] = __shfl_up_sync(0xFFFFFFFFu, w[17], 1);
-        const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w[16], 31), l3 = __shfl_sync(0xFFFFFFFFu, w[17], 31);
+        w[0] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 2], 1);
+        w[1] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 1], 1);
+        const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w[kSegAW - 2], 31), l3 = __shfl_sync(0xFFFFFFFFu, w[kSegAW - 1], 31);
         if (lane == 0) {
             w[0] = pw2;
             w[1] = pw3;
@@ -185,39 +188,38 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
         pw2 = l2;
         pw3 = l3;
         const bool seg_first = it == 0, seg_last = it == its_per_seg - 1;
-        const long long ql = q + 64 * lane;
-        const bool edge = !seg_inside(S, ql, 64);  // stream start / end inside these 64 bytes
-        uint32_t C[18];  // continuation flags (0x80 per byte)
-#pragma unroll
-        for (int k = 0; k < 18; ++k) C[k] = w[k] & 0x80808080u;
+        const long long ql = q + L * lane;
+        const bool edge = !seg_inside(S, ql, L);  // stream start / end inside these bytes
         if (!edge) {
             unsigned nc = 0;
 #pragma unroll
-            for (int k = 2; k < 18; ++k) nc += __popc(C[k]);
-            cnt += 64 - nc;
+            for (int k = 2; k < kSegAW; ++k) nc += __popc(w[k] & 0x80808080u);
+            cnt += L - nc;
         } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < kSegAChunks; ++c) {
                 const uint32_t T16 = hibits16(~w[2 + 4 * c], ~w[3 + 4 * c], ~w[4 + 4 * c], ~w[5 + 4 * c]);
                 cnt += __popc(T16 & seg_inr16(S, ql + 16 * c));
             }
         }
         if (kDelta) {
-            // classes 0/1 for all 16 words (weights 1 / 128 per byte, one dp4a each)
+            // classes 0/1 for every word (weights 1 / 128 per byte, one dp4a each)
             uint32_t hiacc = 0;
 #pragma unroll
-            for (int k = 2; k < 18; ++k) {
-                const uint32_t c1 = __funnelshift_l(C[k - 1], C[k], 8), c2 = __funnelshift_l(C[k - 1], C[k], 16);
+            for (int k = 2; k < kSegAW; ++k) {
+                const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u;
+                const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
                 hiacc |= c1 & c2;
                 sum = __dp4a(w[k] & 0x7F7F7F7Fu, ((c1 >> 7) ^ 0x01010101u) | (c1 & ~c2), sum);
             }
             if (__any_sync(0xFFFFFFFFu, hiacc)) {
                 // integers of 3..5 bytes somewhere in the warp: classes 2..4
 #pragma unroll
-                for (int k = 2; k < 18; ++k) {
-                    const uint32_t c1 = __funnelshift_l(C[k - 1], C[k], 8), c2 = __funnelshift_l(C[k - 1], C[k], 16);
-                    const uint32_t c3 = __funnelshift_l(C[k - 1], C[k], 24), c4 = C[k - 1];
-                    const uint32_t c5 = __funnelshift_l(C[k - 2], C[k - 1], 8);
+                for (int k = 2; k < kSegAW; ++k) {
+                    const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u, cpp = w[k - 2] & 0x80808080u;
+                    const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+                    const uint32_t c3 = __funnelshift_l(cp, ck, 24), c4 = cp;
+                    const uint32_t c5 = __funnelshift_l(cpp, cp, 8);
                     const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
                     sum += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3 & ~c4), 0u) << 14;
                     sum += __dp4a(b, (cc & c3 & c4 & ~c5) >> 7, 0u) << 28;
@@ -229,9 +231,10 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
             }
             if (seg_last && lane == 31) {
                 // tail: bytes after the segment's last terminator (in the last two words)
-                const uint32_t a17 = after_last_terminator(w[17]);
-                const uint32_t a16 = (~w[17] & 0x80808080u) ? 0u : after_last_terminator(w[16]);
-                sum -= word_digit_sum(w[17], w[16], w[15], a17, true) + word_digit_sum(w[16], w[15], w[14], a16, true);
+                const uint32_t a1 = after_last_terminator(w[kSegAW - 1]);
+                const uint32_t a0 = (~w[kSegAW - 1] & 0x80808080u) ? 0u : after_last_terminator(w[kSegAW - 2]);
+                sum -= word_digit_sum(w[kSegAW - 1], w[kSegAW - 2], w[kSegAW - 3], a1, true) +
+                       word_digit_sum(w[kSegAW - 2], w[kSegAW - 3], w[kSegAW - 4], a0, true);
             }
         }
         if (seg_last) {
