@@ -120,6 +120,28 @@ int mvb_shard_carry_device(const unsigned long long *records, int n_ranks, int r
                            int record_words, uint32_t prev, uint32_t *carry_dev,
                            unsigned long long *offset_dev, mvb_stream_t stream);
 
+/* Batched posting lists (BASELINE config 3).  The reference
+ * decodes a batch with one decode_delta_stream call per list
+ * (tools/bench/runner.cpp:28-61); this decodes them all in one launch, one
+ * warp per list.  List l is the byte span in[byte_off[l] .. byte_off[l+1])
+ * holding int_off[l+1] - int_off[l] integers; they land in
+ * out[int_off[l] .. int_off[l+1]), decoded as decode_stream /
+ * decode_delta_stream(span, count, prev[l] (0 if prev == NULL), ...) would,
+ * and results[l] (may be NULL) receives that call's DecodeResult.  byte_off,
+ * int_off (n_lists + 1 entries each), prev, order and results are device
+ * arrays; order (may be NULL) is the order lists are handed out in (longest
+ * first balances best).  Strict mode only (MVB_ERR_INVALID_ARG otherwise:
+ * decode permissive lists one by one).  The workspace needs only the header
+ * (mvb_workspace_bytes(0)).  Asynchronous on `stream`. */
+int mvb_decode_lists_device(const uint8_t *in, size_t in_len, const unsigned long long *byte_off,
+                            const unsigned long long *int_off, size_t n_lists, const unsigned *order,
+                            uint32_t *out, int mode, mvb_result *results, void *ws, size_t ws_bytes,
+                            mvb_stream_t stream);
+int mvb_decode_delta_lists_device(const uint8_t *in, size_t in_len, const unsigned long long *byte_off,
+                                  const unsigned long long *int_off, const uint32_t *prev,
+                                  size_t n_lists, const unsigned *order, uint32_t *out, int mode,
+                                  mvb_result *results, void *ws, size_t ws_bytes, mvb_stream_t stream);
+
 /* ------------------------------------------------------------ host drop-ins */
 
 /* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream

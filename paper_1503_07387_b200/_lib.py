@@ -22,6 +22,8 @@ EXPORTS = (
     "mvb_scan_totals_device",
     "mvb_decode_delta_device_dprev",
     "mvb_shard_carry_device",
+    "mvb_decode_lists_device",
+    "mvb_decode_delta_lists_device",
     "mvb_decode_stream",
     "mvb_decode_delta_stream",
     "mvb_encoded_size",
@@ -67,6 +69,10 @@ def _declare(lib):
     lib.mvb_decode_delta_device_dprev.restype = i32
     lib.mvb_shard_carry_device.argtypes = [vp, i32, i32, i32, u32, vp, vp, vp]
     lib.mvb_shard_carry_device.restype = i32
+    lib.mvb_decode_lists_device.argtypes = [vp, sz, vp, vp, sz, vp, vp, i32, vp, vp, sz, vp]
+    lib.mvb_decode_lists_device.restype = i32
+    lib.mvb_decode_delta_lists_device.argtypes = [vp, sz, vp, vp, vp, sz, vp, vp, i32, vp, vp, sz, vp]
+    lib.mvb_decode_delta_lists_device.restype = i32
     lib.mvb_decode_stream.argtypes = [vp, sz, sz, vp, i32, ctypes.POINTER(MvbResult)]
     lib.mvb_decode_stream.restype = i32
     lib.mvb_decode_delta_stream.argtypes = [vp, sz, sz, u32, vp, i32, ctypes.POINTER(MvbResult)]

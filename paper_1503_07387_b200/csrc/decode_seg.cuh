@@ -264,6 +264,249 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
 
 // ------------------------------------------------------------------ kernel B
 
+// A byte range of a buffer in 16-byte-aligned coordinates: byte q lives at
+// ab[q]; bytes q < lo read as 0x00 (the range start is an integer boundary),
+// bytes q >= hi as 0x80 (no integer ends there).
+struct ByteRange {
+    const uint8_t* ab;
+    long long lo, hi;
+};
+__device__ __forceinline__ uint32_t r_byte(const ByteRange& R, long long q) {
+    if (q < R.lo) return 0x00u;
+    if (q >= R.hi) return 0x80u;
+    return R.ab[q];
+}
+__device__ __forceinline__ uint32_t r_word(const ByteRange& R, long long q) {
+    return r_byte(R, q) | (r_byte(R, q + 1) << 8) | (r_byte(R, q + 2) << 16) | (r_byte(R, q + 3) << 24);
+}
+__device__ __forceinline__ bool r_inside(const ByteRange& R, long long q, long long n) { return q >= R.lo && q + n <= R.hi; }
+__device__ __forceinline__ uint4 r_load16(const ByteRange& R, long long q) {
+    if (r_inside(R, q, 16)) return ldg_stream16(R.ab + q);
+    return make_uint4(r_word(R, q), r_word(R, q + 4), r_word(R, q + 8), r_word(R, q + 12));
+}
+__device__ __forceinline__ uint32_t r_inr16(const ByteRange& R, long long q0) {
+    if (r_inside(R, q0, 16)) return 0xFFFFu;
+    const long long lo = R.lo - q0 > 0 ? R.lo - q0 : 0;
+    const long long hi = R.hi - q0 < 16 ? R.hi - q0 : 16;
+    return (hi <= lo) ? 0u : ((0xFFFFu >> (16 - (hi - lo))) << lo) & 0xFFFFu;
+}
+
+// Where a range decode reports what it saw, as it sees it (nothing stays
+// live in registers across the slice loop): the first malformed integer
+// (output index, range-relative start position) and the end of integer
+// limit-1.  Stream decode: the workspace header (atomics, combined by the last
+// CTA); batched lists: the warp's own shared-memory slots.
+struct RangeSink {
+    WsHeader* hdr;                 // stream: non-null
+    unsigned long long* err_idx;   // lists: warp slot (init ~0ull)
+    long long* err_pos;
+    long long* count_end;          // lists: warp slot (init -1)
+};
+__device__ __forceinline__ void sink_error(const RangeSink& K, unsigned long long idx, long long pos,
+                                           unsigned long long limit) {
+    if (idx >= limit) return;
+    if (K.hdr) {
+        atomicMax(&K.hdr->err_idx_inv, ~idx);
+        atomicMax(&K.hdr->err_pos_inv, ~static_cast<unsigned long long>(pos));
+    } else if (idx < *K.err_idx) {  // one lane, slices in order: no race
+        *K.err_idx = idx;
+        *K.err_pos = pos;
+    }
+}
+__device__ __forceinline__ void sink_count_end(const RangeSink& K, long long pos) {
+    if (K.hdr) K.hdr->count_end = static_cast<unsigned long long>(pos);
+    else *K.count_end = pos;
+}
+
+// What a range decode returns (identical in every lane).
+struct RangeOut {
+    long long last_end;  // -1 if the range holds no integer
+    unsigned long long n;
+};
+
+// One warp decodes the integers ending in slices [qs, qe) (512-byte steps,
+// qs 16-byte aligned) of range R: terminator scan, V digit windows and EP
+// end list in warp-private shared memory, phase 2 (8 integers per lane per
+// pass), in-warp delta prefix from `carry`, and 16-byte-aligned stores to
+// out[base ...] of every integer with output index < limit.
+template <bool kDelta>
+__device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, long long qe, unsigned long long base,
+                                             uint32_t carry, unsigned long long limit, uint32_t* out, char* vbase,
+                                             uint16_t* eph, int lane, const RangeSink& K, RangeOut& ro) {
+    const uint32_t r0 = 8u + 16u * static_cast<uint32_t>(lane);  // V index of this lane's chunk
+    const uintptr_t out_w = reinterpret_cast<uintptr_t>(out) >> 2;
+    unsigned long long run = base;  // output index of the next integer
+    long long last_end = -1;
+    uint32_t pw2 = 0, pw3 = 0;
+    if (lane == 0) {
+        if (r_inside(R, qs - 8, 8)) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(R.ab + qs - 8));
+            pw2 = v.x;
+            pw3 = v.y;
+        } else {
+            pw2 = r_word(R, qs - 8);
+            pw3 = r_word(R, qs - 4);
+        }
+    }
+    uint4 nx = r_load16(R, qs + 16 * lane);  // prefetched slice
+    for (long long q = qs; q < qe; q += kSegSlice) {
+        const long long q0 = q + 16 * lane;
+        const uint4 x = nx;
+        if (q + kSegSlice < qe) nx = r_load16(R, q0 + kSegSlice);
+        const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
+        uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
+        uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
+        const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w2, 31), l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
+        const uint32_t nf = __shfl_sync(0xFFFFFFFFu, nx.x, 0);  // first word of the next slice
+        if (lane == 0) {
+            wp2 = pw2;
+            wp3 = pw3;
+        }
+        if (lane == 31)
+            wn = (q + kSegSlice < qe) ? nf
+                 : r_inside(R, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + q0 + 16))
+                                           : r_word(R, q0 + 16);
+        pw2 = l2;
+        pw3 = l3;
+
+        // ---- phase 1: terminators, counts ----
+        const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
+        const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
+        const uint32_t Cx = ~Tx & 0x0FFFFFFFu;
+        const uint32_t inr16 = r_inr16(R, q0);
+        const uint32_t ends16 = T16 & inr16;
+        const uint32_t n_own = __popc(ends16);
+        uint32_t incl = n_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t wexcl = incl - n_own;
+        // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
+        uint32_t bad16 = 0;
+        if (Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3)) {
+            const uint32_t five = (Tx >> 3) & (Cx >> 4) & (Cx >> 5) & (Cx >> 6) & (Cx >> 7) & inr16;
+            if (five) {
+                const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
+                const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
+                const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
+                const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
+                bad16 = five & hibits16(g0, g1, g2, g3);
+            }
+        }
+        if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the slice's first malformed integer
+            const int j = bad16 ? __ffs(bad16) - 1 : 0;
+            unsigned long long idx = bad16 ? run + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
+            long long pos = q0 + j - 4 - R.lo;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+                const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
+                if (oi < idx) {
+                    idx = oi;
+                    pos = op;
+                }
+            }
+            if (lane == 0) sink_error(K, idx, pos, limit);
+        }
+        if (n_w == 0) continue;  // warp-uniform
+        // end of integer limit-1, if it ends in this slice
+        if (limit - run <= n_w && limit - 1 - run >= wexcl && limit - 1 - run < wexcl + n_own) {
+            uint32_t m = ends16;
+            for (unsigned r = static_cast<unsigned>(limit - 1 - run - wexcl); r > 0; --r) m &= m - 1;
+            sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
+        }
+        if (wexcl + n_own == n_w && n_own) last_end = q0 + (31 - __clz(ends16)) + 1 - R.lo;
+
+        // ---- V digit windows (positions -8 .. 511 of the slice) and EP ends ----
+        const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3), dn = digits4(wn);
+        const uint32_t vo = 4u * r0;
+        *reinterpret_cast<uint4*>(vbase + v_swz(vo)) = vquad(d0, d1);
+        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 16)) = vquad(d1, d2);
+        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 32)) = vquad(d2, d3);
+        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 48)) = vquad(d3, dn);
+        if (lane == 0) {
+            const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
+            *reinterpret_cast<uint4*>(vbase + v_swz(0)) = vquad(dp2, dp3);
+            *reinterpret_cast<uint4*>(vbase + v_swz(16)) = vquad(dp3, d0);
+            const uint32_t tp8 = Tx & 0xFFu;  // positions -8..-1 -> V index 0..7
+            // the range start is an integer boundary: the padding before it
+            // holds no integers (they are masked out of ends16)
+            eph[7] = (q <= R.lo) ? static_cast<uint16_t>(7 + (R.lo - q))
+                                 : static_cast<uint16_t>(tp8 ? 31 - __clz(tp8) : 0xFFFF);
+        }
+        uint16_t* ep = eph + 8 + wexcl;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if ((ends16 >> j) & 1u) {
+                *ep = static_cast<uint16_t>(r0 + j);
+                ++ep;
+            }
+        }
+        if (n_own && wexcl + n_own == n_w) {  // zero-width padding for the last octet
+            const uint16_t rl = static_cast<uint16_t>(r0 + (31 - __clz(ends16)));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ep[k] = rl;
+        }
+        __syncwarp();
+
+        // ---- phase 2 and stores: 8 integers per lane per pass ----
+        for (uint32_t q2 = 0; q2 < n_w; q2 += 256) {
+            const uint32_t u = q2 + 8u * lane;
+            uint32_t val[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) val[k] = 0;
+            if (u < n_w) {
+                const uint4 ea = *reinterpret_cast<const uint4*>(eph + 8 + u);  // 8 ends
+                const uint32_t e[9] = {eph[7 + u], ea.x & 0xFFFFu, ea.x >> 16, ea.y & 0xFFFFu, ea.y >> 16,
+                                       ea.z & 0xFFFFu, ea.z >> 16, ea.w & 0xFFFFu, ea.w >> 16};
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    val[k] = *reinterpret_cast<const uint32_t*>(vbase + v_swz(4u * ((e[k] + 1u) & 0xFFFFu))) &
+                             bmsk(7u * ((e[k + 1] - e[k]) & 0xFFFFu));
+            }
+            if (kDelta) {
+#pragma unroll
+                for (int k = 1; k < 8; ++k) val[k] += val[k - 1];
+                uint32_t xs = val[7];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xs, o);
+                    if (lane >= o) xs += y;
+                }
+                const uint32_t ex = carry + xs - val[7];
+                carry += __shfl_sync(0xFFFFFFFFu, xs, 31);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) val[k] += ex;
+            }
+            const unsigned long long gi = run + q2;  // output index of this pass's first integer
+            if (gi < limit) {
+                const unsigned long long room = limit - gi;
+                const unsigned npass = n_w - q2 < 256u ? n_w - q2 : 256u;
+                const unsigned plim = room < npass ? static_cast<unsigned>(room) : npass;
+                uint32_t* const op = out + gi;
+                switch ((4u - static_cast<unsigned>((out_w + gi) & 3u)) & 3u) {
+                    case 0: store_octets<0>(op, val, lane, plim); break;
+                    case 1: store_octets<1>(op, val, lane, plim); break;
+                    case 2: store_octets<2>(op, val, lane, plim); break;
+                    default: store_octets<3>(op, val, lane, plim); break;
+                }
+            }
+        }
+        run += n_w;
+        __syncwarp();  // V / EP are rewritten by the next slice
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long le = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
+        last_end = le > last_end ? le : last_end;
+    }
+    ro.last_end = last_end;
+    ro.n = run - base;
+}
+
 template <bool kDelta>
 __global__ void __launch_bounds__(kSegThreads) vbyte_seg_decode(SegParams S) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -274,8 +517,7 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_decode(SegParams S) {
     uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const uint32_t r0 = 8u + 16u * static_cast<uint32_t>(lane);  // V index of this lane's chunk
-    const uintptr_t out_w = reinterpret_cast<uintptr_t>(S.out) >> 2;
+    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
 
     for (long long s = gw; s < S.n_seg; s += nw) {
         // ---- output index and carry of the segment: groups before + segments before in the group ----
@@ -295,173 +537,13 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_decode(SegParams S) {
             base += __shfl_xor_sync(0xFFFFFFFFu, base, o);
             if (kDelta) csum += __shfl_xor_sync(0xFFFFFFFFu, csum, o);
         }
-        uint32_t carry = kDelta ? static_cast<uint32_t>(csum) + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
-        unsigned long long run = base;  // output index of the next integer
-        if (run >= S.count) continue;   // nothing of this segment is stored (warp-uniform)
-
-        const long long qs = s * S.seg_bytes;
-        const long long qe = qs + S.seg_bytes;
-        uint32_t pw2 = 0, pw3 = 0;
-        if (lane == 0) {
-            if (seg_inside(S, qs - 8, 8)) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(S.in - S.mis + qs - 8));
-                pw2 = v.x;
-                pw3 = v.y;
-            } else {
-                pw2 = seg_word(S, qs - 8);
-                pw3 = seg_word(S, qs - 4);
-            }
-        }
-        uint4 nx = seg_load16(S, qs + 16 * lane);  // prefetched slice
-        long long last_end = -1;                   // stream position after the segment's last integer
-        for (long long q = qs; q < qe; q += kSegSlice) {
-            const long long q0 = q + 16 * lane;
-            const uint4 x = nx;
-            if (q + kSegSlice < qe) nx = seg_load16(S, q0 + kSegSlice);
-            const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
-            uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
-            uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
-            const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w2, 31), l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
-            const uint32_t nf = __shfl_sync(0xFFFFFFFFu, nx.x, 0);  // first word of the next slice
-            if (lane == 0) {
-                wp2 = pw2;
-                wp3 = pw3;
-            }
-            if (lane == 31)
-                wn = (q + kSegSlice < qe) ? nf
-                     : seg_inside(S, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(S.in - S.mis + q0 + 16))
-                                                 : seg_word(S, q0 + 16);
-            pw2 = l2;
-            pw3 = l3;
-
-            // ---- phase 1: terminators, counts ----
-            const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
-            const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
-            const uint32_t Cx = ~Tx & 0x0FFFFFFFu;
-            const uint32_t inr16 = seg_inr16(S, q0);
-            const uint32_t ends16 = T16 & inr16;
-            const uint32_t n_own = __popc(ends16);
-            uint32_t incl = n_own;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            const uint32_t wexcl = incl - n_own;
-            // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
-            if (Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3)) {
-                const uint32_t five = (Tx >> 3) & (Cx >> 4) & (Cx >> 5) & (Cx >> 6) & (Cx >> 7) & inr16;
-                if (five) {
-                    const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
-                    const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
-                    const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
-                    const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
-                    const uint32_t bad16 = five & hibits16(g0, g1, g2, g3);
-                    if (bad16) {
-                        const int j = __ffs(bad16) - 1;
-                        const unsigned long long idx = run + wexcl + __popc(ends16 & ((1u << j) - 1u));
-                        if (idx < S.count) {
-                            atomicMax(&S.hdr->err_idx_inv, ~idx);
-                            atomicMax(&S.hdr->err_pos_inv, ~static_cast<unsigned long long>(q0 + j - 4 - S.mis));
-                        }
-                    }
-                }
-            }
-            if (n_w == 0) continue;  // warp-uniform
-            // end of integer count-1, if it ends in this slice
-            if (S.count - run <= n_w && S.count - 1 - run >= wexcl && S.count - 1 - run < wexcl + n_own) {
-                uint32_t m = ends16;
-                for (unsigned r = static_cast<unsigned>(S.count - 1 - run - wexcl); r > 0; --r) m &= m - 1;
-                S.hdr->count_end = static_cast<unsigned long long>(q0 + (__ffs(m) - 1) + 1 - S.mis);
-            }
-            if (wexcl + n_own == n_w && n_own) last_end = q0 + (31 - __clz(ends16)) + 1 - S.mis;
-
-            // ---- V digit windows (positions -8 .. 511 of the slice) and EP ends ----
-            const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3), dn = digits4(wn);
-            const uint32_t vo = 4u * r0;
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo)) = vquad(d0, d1);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 16)) = vquad(d1, d2);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 32)) = vquad(d2, d3);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 48)) = vquad(d3, dn);
-            if (lane == 0) {
-                const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
-                *reinterpret_cast<uint4*>(vbase + v_swz(0)) = vquad(dp2, dp3);
-                *reinterpret_cast<uint4*>(vbase + v_swz(16)) = vquad(dp3, d0);
-                const uint32_t tp8 = Tx & 0xFFu;  // positions -8..-1 -> V index 0..7
-                // the stream start is an integer boundary: the padding before it
-                // holds no integers (they are masked out of ends16)
-                eph[7] = (q <= S.mis) ? static_cast<uint16_t>(7 + (S.mis - q))
-                                      : static_cast<uint16_t>(tp8 ? 31 - __clz(tp8) : 0xFFFF);
-            }
-            uint16_t* ep = eph + 8 + wexcl;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if ((ends16 >> j) & 1u) {
-                    *ep = static_cast<uint16_t>(r0 + j);
-                    ++ep;
-                }
-            }
-            if (n_own && wexcl + n_own == n_w) {  // zero-width padding for the last octet
-                const uint16_t rl = static_cast<uint16_t>(r0 + (31 - __clz(ends16)));
-#pragma unroll
-                for (int k = 0; k < 8; ++k) ep[k] = rl;
-            }
-            __syncwarp();
-
-            // ---- phase 2 and stores: 8 integers per lane per pass ----
-            for (uint32_t q2 = 0; q2 < n_w; q2 += 256) {
-                const uint32_t u = q2 + 8u * lane;
-                uint32_t val[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) val[k] = 0;
-                if (u < n_w) {
-                    const uint4 ea = *reinterpret_cast<const uint4*>(eph + 8 + u);  // 8 ends
-                    const uint32_t e[9] = {eph[7 + u], ea.x & 0xFFFFu, ea.x >> 16, ea.y & 0xFFFFu, ea.y >> 16,
-                                           ea.z & 0xFFFFu, ea.z >> 16, ea.w & 0xFFFFu, ea.w >> 16};
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        val[k] = *reinterpret_cast<const uint32_t*>(vbase + v_swz(4u * ((e[k] + 1u) & 0xFFFFu))) &
-                                 bmsk(7u * ((e[k + 1] - e[k]) & 0xFFFFu));
-                }
-                uint32_t ex = 0;
-                if (kDelta) {
-#pragma unroll
-                    for (int k = 1; k < 8; ++k) val[k] += val[k - 1];
-                    uint32_t xs = val[7];
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xs, o);
-                        if (lane >= o) xs += y;
-                    }
-                    ex = carry + xs - val[7];
-                    carry += __shfl_sync(0xFFFFFFFFu, xs, 31);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) val[k] += ex;
-                }
-                const unsigned long long gi = run + q2;  // output index of this pass's first integer
-                if (gi < S.count) {
-                    const unsigned long long room = S.count - gi;
-                    const unsigned npass = n_w - q2 < 256u ? n_w - q2 : 256u;
-                    const unsigned plim = room < npass ? static_cast<unsigned>(room) : npass;
-                    uint32_t* const op = S.out + gi;
-                    switch ((4u - static_cast<unsigned>((out_w + gi) & 3u)) & 3u) {
-                        case 0: store_octets<0>(op, val, lane, plim); break;
-                        case 1: store_octets<1>(op, val, lane, plim); break;
-                        case 2: store_octets<2>(op, val, lane, plim); break;
-                        default: store_octets<3>(op, val, lane, plim); break;
-                    }
-                }
-            }
-            run += n_w;
-            __syncwarp();  // V / EP are rewritten by the next slice
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const long long y = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
-            last_end = y > last_end ? y : last_end;
-        }
-        if (lane == 0 && last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(last_end));
+        if (base >= S.count) continue;  // nothing of this segment is stored (warp-uniform)
+        const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
+        RangeOut ro;
+        const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
+        decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph, lane,
+                             K, ro);
+        if (lane == 0 && ro.last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
     }
 
     // ---- completion; the last CTA produces the DecodeResult ----
@@ -518,6 +600,98 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_decode(SegParams S) {
         h->epoch = h->epoch + 1;
     }
     __threadfence();
+}
+
+// ------------------------------------------------------------------ batched lists
+
+// Independent lists (BASELINE config 3, SURVEY.md §8e "c3: independent
+// units"): list l is the byte span in[byte_off[l] .. byte_off[l+1]) holding
+// int_off[l+1] - int_off[l] integers, decoded -- delta from prev[l] (0 if no
+// prev array) -- into out[int_off[l] ...], exactly as the reference's
+// per-list decode_delta_stream call (tools/bench/runner.cpp:28-61) would.
+// One warp per list, lists handed out by a ticket counter (in `order` if
+// given, e.g. longest first); no cross-list dependency at all.
+struct ListParams {
+    const uint8_t* ab;  // 16-byte-aligned base: in = ab + mis0
+    long long mis0;
+    long long in_len;
+    const unsigned long long* byte_off;  // n_lists + 1
+    const unsigned long long* int_off;   // n_lists + 1
+    const uint32_t* prev;                // n_lists or null
+    const unsigned* order;               // n_lists or null
+    long long n_lists;
+    uint32_t* out;
+    mvb_result* results;  // n_lists or null
+    WsHeader* hdr;
+};
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ bool s_last;
+    __shared__ unsigned long long s_err_idx[kSegWarps];
+    __shared__ long long s_err_pos[kSegWarps], s_count_end[kSegWarps];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * (4 * kSegVW);
+    uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    while (true) {
+        long long k = 0;
+        if (lane == 0) k = static_cast<long long>(atomicAdd(&L.hdr->ticket, 1ull));
+        k = __shfl_sync(0xFFFFFFFFu, k, 0);
+        if (k >= L.n_lists) break;
+        const long long l = L.order ? static_cast<long long>(L.order[k]) : k;
+        long long b0 = static_cast<long long>(L.byte_off[l]), b1 = static_cast<long long>(L.byte_off[l + 1]);
+        if (b1 > L.in_len) b1 = L.in_len;  // never read past in + in_len
+        if (b0 > b1) b0 = b1;
+        const unsigned long long base = L.int_off[l];
+        const unsigned long long cnt = L.int_off[l + 1] > base ? L.int_off[l + 1] - base : 0ull;
+        mvb_result r;
+        r.reserved = 0;
+        if (cnt == 0) {  // decode_test.cpp:204-206: an empty request is OK
+            r.status = MVB_OK;
+            r.values_written = 0;
+            r.bytes_consumed = 0;
+        } else {
+            const ByteRange R = {L.ab, L.mis0 + b0, L.mis0 + b1};
+            if (lane == 0) {
+                s_err_idx[wid] = ~0ull;
+                s_count_end[wid] = -1;
+            }
+            __syncwarp();
+            RangeOut ro;
+            const RangeSink K = {nullptr, &s_err_idx[wid], &s_err_pos[wid], &s_count_end[wid]};
+            decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, kDelta && L.prev ? L.prev[l] : 0u, base + cnt, L.out,
+                                 vbase, eph, lane, K, ro);
+            __syncwarp();
+            const unsigned long long ei = s_err_idx[wid];
+            if (ei != ~0ull && ei < base + cnt) {
+                r.status = MVB_MALFORMED;
+                r.values_written = ei - base;
+                r.bytes_consumed = static_cast<unsigned long long>(s_err_pos[wid]);
+            } else if (ro.n >= cnt) {
+                r.status = MVB_OK;
+                r.values_written = cnt;
+                r.bytes_consumed = static_cast<unsigned long long>(s_count_end[wid]);
+            } else {
+                r.status = MVB_TRUNCATED;
+                r.values_written = ro.n;
+                r.bytes_consumed = ro.last_end >= 0 ? static_cast<unsigned long long>(ro.last_end) : 0ull;
+            }
+        }
+        if (lane == 0 && L.results) L.results[l] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&L.hdr->done, 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        L.hdr->ticket = 0;
+        L.hdr->done = 0;
+        __threadfence();
+    }
 }
 
 }  // namespace mvbk

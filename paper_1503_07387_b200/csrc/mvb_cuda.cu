@@ -451,6 +451,71 @@ int mvb_shard_carry_device(const unsigned long long* records, int n_ranks, int r
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
+}  // extern "C"
+
+namespace {
+template <bool Delta>
+int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                 const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, const unsigned* order,
+                 uint32_t* out, int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (n_lists == 0) return 0;
+    if (byte_off == nullptr || int_off == nullptr || (in == nullptr && in_len > 0)) return MVB_ERR_INVALID_ARG;
+    if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;  // permissive lists: decode each list on its own
+    if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
+    static int per_sm = -1;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return MVB_ERR_CUDA;
+    if (per_sm < 0) {
+        if (cudaFuncSetAttribute(mvbk::vbyte_lists_decode<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kSegSmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_lists_decode<Delta>, mvbk::kSegThreads,
+                                                          mvbk::kSegSmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        per_sm = n > 0 ? n : 1;
+    }
+    mvbk::ListParams L;
+    const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
+    L.ab = in - mis;
+    L.mis0 = static_cast<long long>(mis);
+    L.in_len = static_cast<long long>(in_len);
+    L.byte_off = byte_off;
+    L.int_off = int_off;
+    L.prev = prev;
+    L.order = order;
+    L.n_lists = static_cast<long long>(n_lists);
+    L.out = out;
+    L.results = results_dev;
+    L.hdr = static_cast<WsHeader*>(ws);
+    const long long warps_needed = static_cast<long long>(n_lists);
+    const long long ctas = std::min<long long>(static_cast<long long>(per_sm) * sms,
+                                               (warps_needed + mvbk::kSegWarps - 1) / mvbk::kSegWarps);
+    mvbk::vbyte_lists_decode<Delta><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, mvbk::kSegSmem, s>>>(L);
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" {
+
+int mvb_decode_lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                            const unsigned long long* int_off, size_t n_lists, const unsigned* order, uint32_t* out,
+                            int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, mvb_stream_t stream) {
+    return lists_device<false>(in, in_len, byte_off, int_off, nullptr, n_lists, order, out, mode, results_dev, ws,
+                               ws_bytes, stream);
+}
+
+int mvb_decode_delta_lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                                  const unsigned long long* int_off, const uint32_t* prev, size_t n_lists,
+                                  const unsigned* order, uint32_t* out, int mode, mvb_result* results_dev, void* ws,
+                                  size_t ws_bytes, mvb_stream_t stream) {
+    return lists_device<true>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev, ws,
+                              ws_bytes, stream);
+}
+
 int mvb_decode_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t* out, int mode, mvb_result* res) {
     return decode_host(in, in_len, count, false, 0, out, mode, res);
 }

@@ -211,6 +211,27 @@ class Decoder:
             out.data_ptr() if count else None, int(mode),
             self.res.data_ptr(), self.ws.data_ptr(), self.ws_bytes, self._stream()))
 
+    def decode_lists(self, inp, byte_offsets, int_offsets, out, prev=None, order=None, results=None,
+                     delta: bool = True, mode: int = 0) -> None:
+        """Batched posting lists (mvb_decode[_delta]_lists_device): list l is
+        inp[byte_offsets[l]:byte_offsets[l+1]] with int_offsets[l+1] -
+        int_offsets[l] integers decoded into out[int_offsets[l]:...] (delta from
+        prev[l], default 0).  Offsets are int64 CUDA tensors (n+1 entries);
+        ``results`` (optional, int64 CUDA tensor of n*3) receives each list's
+        DecodeResult as (status, values_written, bytes_consumed)."""
+        n = int(byte_offsets.numel()) - 1
+        L = _lib.lib()
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        if delta:
+            rc = L.mvb_decode_delta_lists_device(ptr(inp) if inp.numel() else None, inp.numel(), byte_offsets.data_ptr(),
+                                                 int_offsets.data_ptr(), ptr(prev), n, ptr(order), ptr(out), int(mode),
+                                                 ptr(results), self.ws.data_ptr(), self.ws_bytes, self._stream())
+        else:
+            rc = L.mvb_decode_lists_device(ptr(inp) if inp.numel() else None, inp.numel(), byte_offsets.data_ptr(),
+                                           int_offsets.data_ptr(), n, ptr(order), ptr(out), int(mode), ptr(results),
+                                           self.ws.data_ptr(), self.ws_bytes, self._stream())
+        _check(rc)
+
     def result(self) -> DecodeResult:
         r = self.res.cpu().numpy().view(np.uint64)
         status = int(np.int64(r[0]) & 0xFFFFFFFF)

@@ -351,3 +351,56 @@ def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
                     assert np.array_equal(out.cpu().numpy().view(np.uint32), oo), (choice, v.size, mode)
     finally:
         _lib.set_kernel_choice(0)
+
+
+@pytest.mark.parametrize("delta", [True, False])
+def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta):
+    """mvb_decode[_delta]_lists_device against one oracle decode per list,
+    including empty lists, count-limited lists (more bytes than integers),
+    truncated and malformed lists, unaligned list starts and a longest-first
+    order."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    parts, counts, prevs = [], [], []
+    for l in range(700):
+        n = int(rng.integers(0, 3000)) if l % 7 else int(rng.integers(0, 4))
+        v = W.mixed_values(n, l + 1) if n else np.zeros(0, np.uint32)
+        e = oracle.encode_sequence(v) if n else np.zeros(0, np.uint8)
+        cnt = n
+        if l % 11 == 3 and n > 2:
+            cnt = n - 2  # span holds more integers than requested
+        if l % 13 == 5 and e.size > 3:
+            e = e[:-1]   # truncated last integer
+        if l % 17 == 9 and e.size > 40:
+            e = e.copy()
+            e[20:26] = 0x80  # over-long run: malformed
+        parts.append(e)
+        counts.append(cnt)
+        prevs.append(int(rng.integers(0, 1 << 32)))
+    byte_off = np.zeros(len(parts) + 1, np.uint64)
+    byte_off[1:] = np.cumsum([p.size for p in parts])
+    int_off = np.zeros(len(parts) + 1, np.uint64)
+    int_off[1:] = np.cumsum(counts)
+    data = np.concatenate([np.zeros(3, np.uint8)] + parts)  # 3-byte offset: unaligned list starts
+    byte_off += 3
+    src = torch.from_numpy(data).to(cuda)
+    out = torch.full((int(int_off[-1]) + 4,), -1, dtype=torch.int32, device=cuda)
+    res = torch.zeros(len(parts) * 3, dtype=torch.int64, device=cuda)
+    order = np.argsort(-np.diff(byte_off).astype(np.int64), kind="stable").astype(np.uint32)
+    d = mvb.Decoder(cuda, 1 << 16)
+    d.decode_lists(src, torch.from_numpy(byte_off.view(np.int64)).to(cuda), torch.from_numpy(int_off.view(np.int64)).to(cuda),
+                   out, prev=torch.from_numpy(np.array(prevs, np.uint32).view(np.int32)).to(cuda) if delta else None,
+                   order=torch.from_numpy(order.view(np.int32)).to(cuda), results=res, delta=delta)
+    got = out.cpu().numpy().view(np.uint32)
+    rr = res.cpu().numpy().reshape(-1, 3)
+    for l, e in enumerate(parts):
+        span = data[int(byte_off[l]):int(byte_off[l + 1])]
+        if delta:
+            ro, oo = oracle.decode_delta(span, counts[l], prevs[l])
+        else:
+            ro, oo = oracle.decode(span, counts[l])
+        assert tuple(int(x) for x in rr[l]) == tuple(ro), (l, rr[l], ro)
+        k = ro[1]
+        np.testing.assert_array_equal(got[int(int_off[l]):int(int_off[l]) + k], oo[:k], err_msg=f"list {l}")
+    assert got[int(int_off[-1]):].tolist() == [0xFFFFFFFF] * 4  # nothing past the last list's output
