@@ -71,6 +71,8 @@ def make_workload(name):
         return W.config1()
     if name == "c2":
         return W.config2()
+    if name == "c3":
+        return W.config3()
     if name == "c4":
         return W.config4()
     if name.startswith("c5"):
@@ -184,6 +186,28 @@ def run_reference(args):
     if rank != 0:
         return
     w = make_workload(args.config)
+    if w.byte_offsets is not None:  # c3: lists split over all host threads, each step a bounded sample
+        threads = os.cpu_count() or 1
+        cpu_lists_rate(w, 0.0, 1, gate=True)
+        t_steps, ints = [], 0
+        for _ in range(args.steps):
+            rate, _, n_ints = cpu_lists_rate(w, 0.5, threads, gate=False)
+            t_steps.append(n_ints / rate)
+            ints += n_ints
+        value = ints / sum(t_steps) / 1e9
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.count, "lists": int(w.byte_offsets.size - 1),
+                       "in_bytes": int(w.encoded.size), "bytes_per_int": w.bytes_per_int},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"each step: ~0.5 s of list decodes (mvb::decode_delta_stream per list, "
+                                       f"lists split over {threads} threads)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     if w.count > (1 << 26):  # bounded sample per thread: the first 2^26 integers of the stream
         from paper_1503_07387_b200 import workload as W
 
@@ -520,6 +544,177 @@ def run_sharded(args):
         dist.destroy_process_group()
 
 
+def cpu_lists_rate(w, seconds, threads, gate=True):
+    """Reference decode of the c3 lists: each host thread decodes its own
+    share of the lists with one mvb::decode_delta_stream per list (the
+    reference's runner.cpp decode_list loop), repeating until `seconds`
+    elapse; returns (ints/s, list decodes done, ints decoded)."""
+    from oracle import RefLib
+
+    ref = RefLib()
+    enc = np.ascontiguousarray(w.encoded)
+    bo = np.ascontiguousarray(w.byte_offsets.astype(np.uint64))
+    io = np.ascontiguousarray(w.int_offsets.astype(np.uint64))
+    out = np.empty(w.count + 16, np.uint32)
+    n = bo.size - 1
+    cuts = np.linspace(0, n, threads + 1).astype(np.int64)
+    if gate:
+        assert ref.decode_delta_lists(enc, bo, io, out, 0, n) == 0
+        assert np.array_equal(out[:w.count], w.expected()), "reference list decode disagrees with ground truth"
+    done = [0] * threads
+    ints = [0] * threads
+    stop_at = [time.perf_counter() + seconds]
+
+    def work(i):
+        lo, hi = int(cuts[i]), int(cuts[i + 1])
+        while True:
+            assert ref.decode_delta_lists(enc, bo, io, out, lo, hi) == 0
+            done[i] += hi - lo
+            ints[i] += int(io[hi] - io[lo])
+            if time.perf_counter() >= stop_at[0]:
+                break
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    return sum(ints) / dt, sum(done), sum(ints)
+
+
+def run_lists(args):
+    """Config 3: 65,536 independent delta-coded posting lists decoded in one
+    launch (mvb_decode_delta_lists_device, one warp per list, longest first).
+    A step decodes the whole batch.  Multi-GPU: replicas (the
+    lists partition with no exchange; each rank decodes a full batch)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_07387_b200 import _lib, mvb
+
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    w = make_workload(args.config)
+    n_lists = w.byte_offsets.size - 1
+    lens = np.diff(w.byte_offsets.astype(np.int64))
+    order_np = np.argsort(-lens, kind="stable").astype(np.uint32)
+    h_in = torch.from_numpy(w.encoded).pin_memory()
+    h_bo = torch.from_numpy(w.byte_offsets.astype(np.uint64).view(np.int64)).pin_memory()
+    h_io = torch.from_numpy(w.int_offsets.astype(np.uint64).view(np.int64)).pin_memory()
+    src, bo, io = h_in.to(dev), h_bo.to(dev), h_io.to(dev)
+    order = torch.from_numpy(order_np.view(np.int32)).to(dev)
+    out = torch.empty(w.count, dtype=torch.int32, device=dev)
+    res = torch.zeros(n_lists * 3, dtype=torch.int64, device=dev)
+    d = mvb.Decoder(dev, 1 << 12)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        d.decode_lists(src, bo, io, out, order=order, results=res, delta=True)
+
+    step()
+    torch.cuda.synchronize()
+    rr = res.cpu().numpy().reshape(-1, 3)
+    assert (rr[:, 0] == 0).all() and (rr[:, 1] == np.diff(w.int_offsets.astype(np.int64))).all(), "list results"
+    assert torch.equal(out, torch.from_numpy(w.expected().view(np.int32)).to(dev)), "batched list decode mismatch"
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for s_ in range(args.steps):
+            ev[s_][0].record(stream)
+            step()
+            ev[s_][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(stop)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * w.count * args.steps / (total_ms / 1e3) / 1e9
+    meta = (n_lists + 1) * 16 + n_lists * 4 + n_lists * 24  # offsets, order, results
+    alg_bytes = int(w.encoded.size) + 4 * w.count + meta
+    achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+
+    # end to end: H2D of stream + offsets, the batched decode, D2H of every list's values
+    h_out = torch.empty(w.count, dtype=torch.int32).pin_memory()
+
+    def e2e_step():
+        src.copy_(h_in, non_blocking=True)
+        bo.copy_(h_bo, non_blocking=True)
+        io.copy_(h_io, non_blocking=True)
+        step()
+        h_out.copy_(out, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = world * w.count * e_steps / float(et.item()) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        try:
+            threads = os.cpu_count() or 1
+            rate, lists_done, ints_done = cpu_lists_rate(w, args.cpu_seconds, threads)
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{lists_done} list decodes ({ints_done} ints) of the {w.name} batch by the reference "
+                             f"library's decode_delta_stream, one call per list (runner.cpp decode_list), lists "
+                             f"split over {threads} host threads, ~{args.cpu_seconds:.0f} s"}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": w.name, "n": w.count, "lists": n_lists, "in_bytes": int(w.encoded.size),
+                       "bytes_per_int": round(w.bytes_per_int, 4), "delta": True,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 ({(int(w.encoded.size) + 4 * w.count) / 1e6:.0f} MB > 126 MB)"},
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": load_ncu_traffic(w.name), "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                         "kernel_ms_avg": statistics.mean(kern_ms), "kernel_ms_min": min(kern_ms),
+                         "kernel": "vbyte_lists_decode (one launch per batch)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(w.encoded.size) + 2 * (n_lists + 1) * 8,
+                    "d2h_bytes_per_step": 4 * w.count, "api": "Decoder.decode_lists (mvb_decode_delta_lists_device)"},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def cpu_reference_sample(w, seconds, threads):
     """Reference decode rate on a bounded prefix of a large stream (2^26
     integers, the reference's l1-style chunk of the same bytes)."""
@@ -547,6 +742,8 @@ def main():
         run_reference(args)
     elif args.config == "c4":
         run_sharded(args)
+    elif args.config == "c3":
+        run_lists(args)
     else:
         run_ours(args)
 

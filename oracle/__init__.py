@@ -127,6 +127,8 @@ class RefLib:
         L.mvbref_decode_stream.argtypes = [vp, sz, sz, vp, i32, i32, sz]; L.mvbref_decode_stream.restype = Result
         L.mvbref_decode_delta_stream.argtypes = [vp, sz, sz, u32, vp, i32, i32, sz]
         L.mvbref_decode_delta_stream.restype = Result
+        L.mvbref_decode_delta_lists.argtypes = [vp, vp, vp, vp, sz, sz]
+        L.mvbref_decode_delta_lists.restype = sz
         self.L = L
 
     @staticmethod
@@ -171,6 +173,11 @@ class RefLib:
         out = np.zeros(max(count, 0) + 4, np.uint32) if out is None else out
         r = self.L.mvbref_decode_stream(_p(src), src.size, count, _p(out), mode, path, handoff)
         return r.tuple(), out[:count]
+
+    def decode_delta_lists(self, data, byte_off, int_off, out, lo: int, hi: int) -> int:
+        """Lists [lo, hi) of a batch, one reference decode_delta_stream per
+        list (prev 0); returns the number of lists not OK.  Releases the GIL."""
+        return int(self.L.mvbref_decode_delta_lists(_p(data), _p(byte_off), _p(int_off), _p(out), lo, hi))
 
     def decode_delta_stream(self, data, count: int, prev: int, mode: int = STRICT, path: int = 0,
                             handoff: int = 0, out: Optional[np.ndarray] = None):

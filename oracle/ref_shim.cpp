@@ -15,6 +15,8 @@
 //   mvbref_decode_stream       core/src/decode.cpp:73-82  (auto path: SSE if present)
 //   mvbref_decode_delta_stream core/src/decode.cpp:88-97
 //   mvbref_vector_available    core/src/decode.cpp:28-34
+//   mvbref_decode_delta_lists  one decode_delta_stream call per list, as
+//                              tools/bench/runner.cpp:28-61 decode_list does
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -93,6 +95,20 @@ mvbref_result mvbref_decode_delta_stream(const uint8_t* in, size_t len, size_t c
                                          size_t handoff) {
     return pack(mvb::decode_delta_stream(std::span<const uint8_t>(in, len), count, prev, out,
                                          opts(mode, path, handoff)));
+}
+
+// Lists [lo, hi) of a batch (byte / integer offsets, n_lists + 1 entries):
+// the reference's per-list loop; returns the number of lists not OK.
+size_t mvbref_decode_delta_lists(const uint8_t* in, const uint64_t* byte_off, const uint64_t* int_off,
+                                 uint32_t* out, size_t lo, size_t hi) {
+    size_t bad = 0;
+    for (size_t l = lo; l < hi; ++l) {
+        const auto r = mvb::decode_delta_stream(
+            std::span<const uint8_t>(in + byte_off[l], byte_off[l + 1] - byte_off[l]),
+            int_off[l + 1] - int_off[l], 0, out + int_off[l], mvb::DecodeOptions{});
+        if (r.status != mvb::DecodeStatus::ok) ++bad;
+    }
+    return bad;
 }
 
 }  // extern "C"
