@@ -168,6 +168,21 @@ size_t mvb_encode_sequence(const uint32_t *values, size_t n, uint8_t *out);
 int mvb_encode_deltas(const uint32_t *sorted_values, size_t n, uint8_t *out, size_t *out_len,
                       size_t *bad_index);
 
+/* Device-side encoder (vbyte.cpp:17-45).  Encodes n
+ * device values into out (device, capacity >= 5n bytes, or the exact length
+ * from a previous call) and writes the byte count to *len_dev.  The workspace
+ * (any contents) must hold mvb_encode_workspace_bytes(n) bytes.  Asynchronous
+ * on `stream`.  The deltas form encodes the gaps x[i] - x[i-1] (x[-1] = 0) and
+ * writes to *bad_index_dev the first index where the input decreases, or
+ * ~0ull if it never does (the reference throws std::invalid_argument there,
+ * vbyte.cpp:80-81; the encoded bytes are then unspecified). */
+size_t mvb_encode_workspace_bytes(size_t n);
+int mvb_encode_sequence_device(const uint32_t *values, size_t n, uint8_t *out, unsigned long long *len_dev,
+                               void *ws, size_t ws_bytes, mvb_stream_t stream);
+int mvb_encode_deltas_device(const uint32_t *sorted_values, size_t n, uint8_t *out,
+                             unsigned long long *len_dev, unsigned long long *bad_index_dev, void *ws,
+                             size_t ws_bytes, mvb_stream_t stream);
+
 /* Library build/version string. */
 const char *mvb_version(void);
 

@@ -24,6 +24,9 @@ EXPORTS = (
     "mvb_shard_carry_device",
     "mvb_decode_lists_device",
     "mvb_decode_delta_lists_device",
+    "mvb_encode_workspace_bytes",
+    "mvb_encode_sequence_device",
+    "mvb_encode_deltas_device",
     "mvb_decode_stream",
     "mvb_decode_delta_stream",
     "mvb_encoded_size",
@@ -73,6 +76,12 @@ def _declare(lib):
     lib.mvb_decode_lists_device.restype = i32
     lib.mvb_decode_delta_lists_device.argtypes = [vp, sz, vp, vp, vp, sz, vp, vp, i32, vp, vp, sz, vp]
     lib.mvb_decode_delta_lists_device.restype = i32
+    lib.mvb_encode_workspace_bytes.argtypes = [sz]
+    lib.mvb_encode_workspace_bytes.restype = sz
+    lib.mvb_encode_sequence_device.argtypes = [vp, sz, vp, vp, vp, sz, vp]
+    lib.mvb_encode_sequence_device.restype = i32
+    lib.mvb_encode_deltas_device.argtypes = [vp, sz, vp, vp, vp, vp, sz, vp]
+    lib.mvb_encode_deltas_device.restype = i32
     lib.mvb_decode_stream.argtypes = [vp, sz, sz, vp, i32, ctypes.POINTER(MvbResult)]
     lib.mvb_decode_stream.restype = i32
     lib.mvb_decode_delta_stream.argtypes = [vp, sz, sz, u32, vp, i32, ctypes.POINTER(MvbResult)]

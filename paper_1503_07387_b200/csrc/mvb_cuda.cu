@@ -20,6 +20,7 @@
 #include "decode_seg.cuh"
 #include "decode_warp.cuh"
 #include "totals_kernel.cuh"
+#include "encode_kernel.cuh"
 
 namespace {
 
@@ -514,6 +515,42 @@ int mvb_decode_delta_lists_device(const uint8_t* in, size_t in_len, const unsign
                                   size_t ws_bytes, mvb_stream_t stream) {
     return lists_device<true>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev, ws,
                               ws_bytes, stream);
+}
+
+size_t mvb_encode_workspace_bytes(size_t n) {
+    return ((n + mvbk::kEncTile - 1) / mvbk::kEncTile + 1) * sizeof(unsigned long long);
+}
+
+}  // extern "C"
+
+namespace {
+template <bool Delta>
+int encode_device(const uint32_t* values, size_t n, uint8_t* out, unsigned long long* len_dev,
+                  unsigned long long* bad_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (len_dev == nullptr || (n > 0 && (values == nullptr || out == nullptr))) return MVB_ERR_INVALID_ARG;
+    if (Delta && bad_dev == nullptr) return MVB_ERR_INVALID_ARG;
+    if (Delta && cudaMemsetAsync(bad_dev, 0xFF, sizeof(unsigned long long), s) != cudaSuccess) return MVB_ERR_CUDA;
+    if (n == 0) return cudaMemsetAsync(len_dev, 0, sizeof(unsigned long long), s) == cudaSuccess ? 0 : MVB_ERR_CUDA;
+    const size_t tiles = (n + mvbk::kEncTile - 1) / mvbk::kEncTile;
+    if (ws == nullptr || ws_bytes < tiles * sizeof(unsigned long long)) return MVB_ERR_WORKSPACE;
+    unsigned long long* tb = static_cast<unsigned long long*>(ws);
+    mvbk::vbyte_enc_sizes<Delta><<<static_cast<unsigned>(tiles), mvbk::kEncThreads, 0, s>>>(values, n, tb, bad_dev);
+    mvbk::vbyte_enc_scan<<<1, 1024, 0, s>>>(tb, tiles, len_dev);
+    mvbk::vbyte_enc_write<Delta><<<static_cast<unsigned>(tiles), mvbk::kEncThreads, 0, s>>>(values, n, tb, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" {
+
+int mvb_encode_sequence_device(const uint32_t* values, size_t n, uint8_t* out, unsigned long long* len_dev, void* ws,
+                               size_t ws_bytes, mvb_stream_t stream) {
+    return encode_device<false>(values, n, out, len_dev, nullptr, ws, ws_bytes, stream);
+}
+
+int mvb_encode_deltas_device(const uint32_t* sorted_values, size_t n, uint8_t* out, unsigned long long* len_dev,
+                             unsigned long long* bad_index_dev, void* ws, size_t ws_bytes, mvb_stream_t stream) {
+    return encode_device<true>(sorted_values, n, out, len_dev, bad_index_dev, ws, ws_bytes, stream);
 }
 
 int mvb_decode_stream(const uint8_t* in, size_t in_len, size_t count, uint32_t* out, int mode, mvb_result* res) {

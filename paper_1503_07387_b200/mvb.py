@@ -309,5 +309,31 @@ def decode_delta_scalar(inp, count, prev, out, mode: DecodeMode = DecodeMode.str
     return _decode(inp, count, prev, out, mode, delta=True)
 
 
+def encode_device(values, deltas: bool = False):
+    """Device-side encode_sequence / encode_deltas (mvb_encode_*_device) of a
+    uint32/int32 CUDA tensor; returns a uint8 CUDA tensor of the encoded
+    bytes.  Synchronises to read the length; raises ValueError (as the
+    reference's encode_deltas) if `deltas` and the input decreases."""
+    import torch
+
+    n = int(values.numel())
+    dev = values.device
+    L = _lib.lib()
+    ws = torch.empty(max(int(L.mvb_encode_workspace_bytes(n)), 8), dtype=torch.uint8, device=dev)
+    out = torch.empty(max(5 * n, 1), dtype=torch.uint8, device=dev)
+    meta = torch.zeros(2, dtype=torch.int64, device=dev)  # length, first decreasing index
+    stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    if deltas:
+        _check(L.mvb_encode_deltas_device(values.data_ptr() if n else None, n, out.data_ptr(), meta.data_ptr(),
+                                          meta.data_ptr() + 8, ws.data_ptr(), ws.numel(), stream))
+    else:
+        _check(L.mvb_encode_sequence_device(values.data_ptr() if n else None, n, out.data_ptr(), meta.data_ptr(),
+                                            ws.data_ptr(), ws.numel(), stream))
+    m = meta.cpu().numpy().view(np.uint64)
+    if deltas and n and int(m[1]) != 0xFFFFFFFFFFFFFFFF:
+        raise ValueError(f"encode_deltas: input decreases at index {int(m[1])}")
+    return out[:int(m[0])]
+
+
 def version() -> str:
     return _lib.lib().mvb_version().decode()

@@ -404,3 +404,31 @@ def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta):
         k = ro[1]
         np.testing.assert_array_equal(got[int(int_off[l]):int(int_off[l]) + k], oo[:k], err_msg=f"list {l}")
     assert got[int(int_off[-1]):].tolist() == [0xFFFFFFFF] * 4  # nothing past the last list's output
+
+
+def test_device_encoder_matches_reference_encoder(cuda, oracle):
+    """mvb_encode_sequence_device / mvb_encode_deltas_device byte-for-byte
+    against the reference encoder, across sizes and tile edges; decreasing
+    input reports the first bad index like encode_deltas throws."""
+    import torch
+
+    for n in (0, 1, 5, 4095, 4096, 4097, 100003, 1 << 20):
+        v = W.mixed_values(n, n + 3) if n else np.zeros(0, np.uint32)
+        got = mvb.encode_device(torch.from_numpy(v.view(np.int32)).to(cuda)).cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.encode_sequence(v), err_msg=f"n={n}")
+        s = np.sort(v)
+        got = mvb.encode_device(torch.from_numpy(s.view(np.int32)).to(cuda), deltas=True).cpu().numpy()
+        gaps = np.diff(np.concatenate([[0], s.astype(np.int64)])).astype(np.uint32)
+        np.testing.assert_array_equal(got, oracle.encode_sequence(gaps), err_msg=f"deltas n={n}")
+    v = np.sort(W.mixed_values(50000, 1))
+    v[31337] = v[31336] - 1 if v[31336] else 5
+    v[40000] = 0
+    with pytest.raises(ValueError, match="index 31337" if v[31336] else "index"):
+        mvb.encode_device(torch.from_numpy(v.view(np.int32)).to(cuda), deltas=True)
+    # round trip through the device decoder
+    w = W.config2(1 << 20)
+    enc = mvb.encode_device(torch.from_numpy(w.values.view(np.int32)).to(cuda))
+    out = torch.empty(w.count, dtype=torch.int32, device=cuda)
+    d = mvb.Decoder(cuda, enc.numel())
+    d.decode_delta(enc, w.count, 0, out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), w.expected())
