@@ -309,6 +309,39 @@ def decode_delta_scalar(inp, count, prev, out, mode: DecodeMode = DecodeMode.str
     return _decode(inp, count, prev, out, mode, delta=True)
 
 
+def decode_list(buf, out, buffer_mode: str = "full", buffer_ints: int = 4096, options=None):
+    """One delta-coded list, as the reference benchmark runner's decode_list
+    (tools/bench/runner.cpp:28-61) does it: "full" decodes the whole list in
+    one call; "l1" walks the stream in buffer_ints-integer chunks through a
+    reused buffer, carrying bytes_consumed and the running prefix (prev = the
+    chunk's last value) into the next call -- the chunked caller pattern the
+    drop-in must serve unchanged.  `out` receives the
+    whole list (full) or, for l1, each chunk is copied out of the reused
+    buffer into it (the reference only keeps the buffer).  Returns the
+    DecodeResult of the last call."""
+    if not isinstance(buf, EncodedBuffer):
+        raise MvbError("decode_list takes an EncodedBuffer")
+    if buffer_mode == "full":
+        return decode_delta_stream(buf.bytes, buf.count, 0, out, options)
+    if buffer_mode != "l1":
+        raise MvbError("buffer_mode must be 'full' or 'l1'")
+    data = _u8(buf.bytes)
+    scratch = np.zeros(max(int(buffer_ints), 1), np.uint32)
+    done = offset = 0
+    prev = 0
+    r = DecodeResult()
+    while done < buf.count:
+        n = min(int(buffer_ints), buf.count - done)
+        r = decode_delta_stream(data[offset:], n, prev, scratch, options)
+        if r.status != DecodeStatus.ok:
+            return r
+        offset += r.bytes_consumed
+        prev = int(scratch[n - 1])
+        out[done:done + n] = scratch[:n]
+        done += n
+    return r
+
+
 def encode_device(values, deltas: bool = False):
     """Device-side encode_sequence / encode_deltas (mvb_encode_*_device) of a
     uint32/int32 CUDA tensor; returns a uint8 CUDA tensor of the encoded

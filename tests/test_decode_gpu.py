@@ -432,3 +432,21 @@ def test_device_encoder_matches_reference_encoder(cuda, oracle):
     d = mvb.Decoder(cuda, enc.numel())
     d.decode_delta(enc, w.count, 0, out)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), w.expected())
+
+
+@pytest.mark.parametrize("buffer_ints", [1, 7, 4096])
+def test_chunked_l1_mode_equals_full(oracle, buffer_ints):
+    """The reference runner's l1 buffer mode (chunks of buffer_ints through a
+    reused buffer, bytes_consumed and prev carried across calls) through the
+    GPU drop-in equals one full decode (runner.cpp:28-61)."""
+    rng = np.random.default_rng(buffer_ints)
+    for n in (1, 4095, 4096, 50001):
+        ids = np.unique(rng.integers(0, 1 << 25, n, dtype=np.int64)).astype(np.uint32)
+        buf = mvb.encode_deltas(ids)
+        full = np.zeros(ids.size, np.uint32)
+        l1 = np.zeros(ids.size, np.uint32)
+        assert mvb.decode_list(buf, full, "full").status == mvb.DecodeStatus.ok
+        r = mvb.decode_list(buf, l1, "l1", buffer_ints)
+        assert r.status == mvb.DecodeStatus.ok
+        np.testing.assert_array_equal(full, ids)
+        np.testing.assert_array_equal(l1, ids)
