@@ -129,6 +129,10 @@ class RefLib:
         L.mvbref_decode_delta_stream.restype = Result
         L.mvbref_decode_delta_lists.argtypes = [vp, vp, vp, vp, sz, sz]
         L.mvbref_decode_delta_lists.restype = sz
+        L.mvbref_write_list_file.argtypes = [ctypes.c_char_p, vp, sz, u32, i32]
+        L.mvbref_write_list_file.restype = i32
+        L.mvbref_read_list_file.argtypes = [ctypes.c_char_p, i32, vp, sz, ctypes.POINTER(u32), ctypes.POINTER(i32)]
+        L.mvbref_read_list_file.restype = ctypes.c_longlong
         self.L = L
 
     @staticmethod
@@ -173,6 +177,21 @@ class RefLib:
         out = np.zeros(max(count, 0) + 4, np.uint32) if out is None else out
         r = self.L.mvbref_decode_stream(_p(src), src.size, count, _p(out), mode, path, handoff)
         return r.tuple(), out[:count]
+
+    def write_list_file(self, path, payload, count: int, delta: bool) -> int:
+        b = _u8(payload)
+        return int(self.L.mvbref_write_list_file(str(path).encode(), _p(b), b.size, count, int(delta)))
+
+    def read_list_file(self, path, validate: bool = True):
+        """(payload, count, delta) or None on the reference's ListFileError."""
+        cap = max(os.path.getsize(path), 1)
+        out = np.zeros(cap, np.uint8)
+        cnt, dl = ctypes.c_uint32(0), ctypes.c_int32(0)
+        n = int(self.L.mvbref_read_list_file(str(path).encode(), int(validate), _p(out), cap, ctypes.byref(cnt),
+                                             ctypes.byref(dl)))
+        if n < 0:
+            return None
+        return out[:n], int(cnt.value), bool(dl.value)
 
     def decode_delta_lists(self, data, byte_off, int_off, out, lo: int, hi: int) -> int:
         """Lists [lo, hi) of a batch, one reference decode_delta_stream per

@@ -15,8 +15,11 @@
 //   mvbref_decode_stream       core/src/decode.cpp:73-82  (auto path: SSE if present)
 //   mvbref_decode_delta_stream core/src/decode.cpp:88-97
 //   mvbref_vector_available    core/src/decode.cpp:28-34
+//   mvbref_write_list_file     core/src/list_file.cpp:57-65
+//   mvbref_read_list_file      core/src/list_file.cpp:89-93 (-1 on ListFileError)
 //   mvbref_decode_delta_lists  one decode_delta_stream call per list, as
 //                              tools/bench/runner.cpp:28-61 decode_list does
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -24,6 +27,7 @@
 #include <vector>
 
 #include "mvb/decode.hpp"
+#include "mvb/list_file.hpp"
 #include "mvb/vbyte.hpp"
 
 extern "C" {
@@ -95,6 +99,33 @@ mvbref_result mvbref_decode_delta_stream(const uint8_t* in, size_t len, size_t c
                                          size_t handoff) {
     return pack(mvb::decode_delta_stream(std::span<const uint8_t>(in, len), count, prev, out,
                                          opts(mode, path, handoff)));
+}
+
+int mvbref_write_list_file(const char* path, const uint8_t* bytes, size_t len, uint32_t count, int delta) {
+    try {
+        mvb::EncodedBuffer b;
+        b.bytes.assign(bytes, bytes + len);
+        b.count = count;
+        b.delta_coded = delta != 0;
+        mvb::write_list_file(path, b);
+        return 0;
+    } catch (const mvb::ListFileError&) {
+        return 1;
+    }
+}
+
+// Payload length (bytes copied into out, up to cap), or -1 on ListFileError.
+long long mvbref_read_list_file(const char* path, int validate, uint8_t* out, size_t cap, uint32_t* count,
+                                int* delta) {
+    try {
+        const mvb::EncodedBuffer b = mvb::read_list_file(path, validate != 0);
+        *count = b.count;
+        *delta = b.delta_coded ? 1 : 0;
+        std::memcpy(out, b.bytes.data(), std::min(cap, b.bytes.size()));
+        return static_cast<long long>(b.bytes.size());
+    } catch (const mvb::ListFileError&) {
+        return -1;
+    }
 }
 
 // Lists [lo, hi) of a batch (byte / integer offsets, n_lists + 1 entries):
