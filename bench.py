@@ -728,6 +728,48 @@ def cpu_reference_sample(w, seconds, threads):
                         f"{threads} thread(s), ~{seconds:.0f} s")
 
 
+def run_csv(args):
+    """Reference-schema CSV (K,bits_per_int,scheme,mis,ratio_vs_scalar,
+    buffer_mode): `cuda` rows from the batched GPU decode
+    (paper_1503_07387_b200/bench_csv.py) next to the reference library's own
+    `scalar` and `masked` rows (oracle/_ref, the CPU leg), l1 (4096-integer
+    buffer) and full modes, timed like runner.cpp:174-196."""
+    from oracle import RefLib
+    from paper_1503_07387_b200 import bench_csv as B
+    from paper_1503_07387_b200 import mvb
+
+    ref = RefLib()
+    rows = []
+    for k in range(args.k_min, args.k_max + 1):
+        bufs = [mvb.encode_deltas(ids) for ids in B.group_lists(k, args.lists, args.seed)]
+        ints = sum(b.count for b in bufs)
+        bits = 8.0 * sum(b.bytes.size for b in bufs) / ints
+        out = np.zeros(max(max(b.count for b in bufs), 4096) + 16, np.uint32)
+        for scheme in ("scalar", "masked"):
+            dec = ref.decode_delta_scalar if scheme == "scalar" else ref.decode_delta_stream
+            for mode in ("l1", "full"):
+                def one_pass(dec=dec, mode=mode):
+                    for b in bufs:
+                        if mode == "full":
+                            dec(b.bytes, b.count, 0, out=out)
+                            continue
+                        done = off = prev = 0
+                        while done < b.count:  # runner.cpp:35-44 / :51-60
+                            n = min(4096, b.count - done)
+                            r, _ = dec(b.bytes[off:], n, prev, out=out)
+                            off += r[2]
+                            prev = int(out[n - 1])
+                            done += n
+                rows.append(B.BenchResult(k, bits, scheme, B.time_passes(one_pass, args.min_ms / 1e3, args.reps, ints,
+                                                                         B.wall_timer), 0.0, mode))
+    rows += B.cuda_rows(args.k_min, args.k_max, args.lists, args.seed, args.reps, args.min_ms)
+    rows.sort(key=lambda r: (r.k, r.buffer_mode != "l1", r.scheme))
+    B.add_ratios(rows)
+    with open(args.csv, "w") as f:
+        B.write_csv(f, rows)
+    B.write_csv(sys.stdout, rows)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -737,8 +779,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--preroll", type=float, default=1.0)
+    ap.add_argument("--csv", default=None, help="write the reference-schema CSV (cuda / scalar / masked rows) here")
+    ap.add_argument("--k-min", type=int, default=4)
+    ap.add_argument("--k-max", type=int, default=16)
+    ap.add_argument("--lists", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--min-ms", type=int, default=100)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.csv:
+        run_csv(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.config == "c4":
         run_sharded(args)
