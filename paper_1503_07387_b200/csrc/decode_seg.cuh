@@ -508,7 +508,7 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 }
 
 template <bool kDelta>
-__global__ void __launch_bounds__(kSegThreads) vbyte_seg_decode(SegParams S) {
+__global__ void __launch_bounds__(kSegThreads, 8) vbyte_seg_decode(SegParams S) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
     const int lane = threadIdx.x & 31;
