@@ -36,8 +36,9 @@ namespace mvbk {
 constexpr int kSegWarps = 4;  // warps per CTA
 constexpr int kSegThreads = 32 * kSegWarps;
 constexpr int kSegSlice = 512;
-constexpr int kSegVW = 528;   // V words per warp (8 halo + 512 + pad to 64 B)
-constexpr int kSegEPH = 536;  // EP halfwords per warp: [7] previous end, [8 + k] ends, 8 padding (16-B multiple)
+constexpr int kSegGroup = 2;  // slices scanned before one phase 2 (fills its passes: ~341 ints/slice on c2)
+constexpr int kSegVW = 8 + kSegGroup * 512 + 8;   // V words per warp: 8 halo + the group's positions + pad (64-B multiple)
+constexpr int kSegEPH = 8 + kSegGroup * 512 + 8;  // EP halfwords per warp: [7] previous end, [8 + k] ends, padding
 constexpr int kSegSmem = kSegWarps * (4 * kSegVW + 2 * kSegEPH);
 static_assert((4 * kSegVW) % 64 == 0 && (2 * kSegEPH) % 16 == 0, "alignment");
 
@@ -326,8 +327,10 @@ struct RangeOut {
 
 // One warp decodes the integers ending in slices [qs, qe) (512-byte steps,
 // qs 16-byte aligned) of range R: terminator scan, V digit windows and EP
-// end list in warp-private shared memory, phase 2 (8 integers per lane per
-// pass), in-warp delta prefix from `carry`, and 16-byte-aligned stores to
+// end list in warp-private shared memory for kSegGroup slices at a time, then
+// one phase 2 over the group's integers (8 per lane per pass: two slices'
+// ~682 integers of c2 fill three passes to 89% instead of two to 67%),
+// in-warp delta prefix from `carry`, and 16-byte-aligned stores to
 // out[base ...] of every integer with output index < limit.
 template <bool kDelta>
 __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, long long qe, unsigned long long base,
@@ -349,116 +352,129 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
         }
     }
     uint4 nx = r_load16(R, qs + 16 * lane);  // prefetched slice
-    for (long long q = qs; q < qe; q += kSegSlice) {
-        const long long q0 = q + 16 * lane;
-        const uint4 x = nx;
-        if (q + kSegSlice < qe) nx = r_load16(R, q0 + kSegSlice);
-        const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
-        uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
-        uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
-        const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w2, 31), l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
-        const uint32_t nf = __shfl_sync(0xFFFFFFFFu, nx.x, 0);  // first word of the next slice
-        if (lane == 0) {
-            wp2 = pw2;
-            wp3 = pw3;
-        }
-        if (lane == 31)
-            wn = (q + kSegSlice < qe) ? nf
-                 : r_inside(R, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + q0 + 16))
-                                           : r_word(R, q0 + 16);
-        pw2 = l2;
-        pw3 = l3;
-
-        // ---- phase 1: terminators, counts ----
-        const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
-        const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
-        const uint32_t Cx = ~Tx & 0x0FFFFFFFu;
-        const uint32_t inr16 = r_inr16(R, q0);
-        const uint32_t ends16 = T16 & inr16;
-        const uint32_t n_own = __popc(ends16);
-        uint32_t incl = n_own;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const uint32_t wexcl = incl - n_own;
-        // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
-        uint32_t bad16 = 0;
-        if (Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3)) {
-            const uint32_t five = (Tx >> 3) & (Cx >> 4) & (Cx >> 5) & (Cx >> 6) & (Cx >> 7) & inr16;
-            if (five) {
-                const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
-                const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
-                const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
-                const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
-                bad16 = five & hibits16(g0, g1, g2, g3);
+    for (long long qg = qs; qg < qe; qg += kSegGroup * kSegSlice) {
+        // ---- scan up to kSegGroup slices into one V / EP window ----
+        uint32_t n_g = 0;  // integers of the group so far (warp-uniform)
+#pragma unroll 1
+        for (int h = 0; h < kSegGroup; ++h) {
+            const long long q = qg + h * kSegSlice;
+            if (q >= qe) break;
+            const long long q0 = q + 16 * lane;
+            const uint4 x = nx;
+            if (q + kSegSlice < qe) nx = r_load16(R, q0 + kSegSlice);
+            const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
+            uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
+            uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
+            const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w2, 31), l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
+            const uint32_t nf = __shfl_sync(0xFFFFFFFFu, nx.x, 0);  // first word of the next slice
+            if (lane == 0) {
+                wp2 = pw2;
+                wp3 = pw3;
             }
-        }
-        if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the slice's first malformed integer
-            const int j = bad16 ? __ffs(bad16) - 1 : 0;
-            unsigned long long idx = bad16 ? run + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
-            long long pos = q0 + j - 4 - R.lo;
+            if (lane == 31)
+                wn = (q + kSegSlice < qe) ? nf
+                     : r_inside(R, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + q0 + 16))
+                                               : r_word(R, q0 + 16);
+            pw2 = l2;
+            pw3 = l3;
+
+            // ---- phase 1: terminators, counts ----
+            const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
+            const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
+            const uint32_t Cx = ~Tx & 0x0FFFFFFFu;
+            const uint32_t inr16 = r_inr16(R, q0);
+            const uint32_t ends16 = T16 & inr16;
+            const uint32_t n_own = __popc(ends16);
+            uint32_t incl = n_own;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
-                const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
-                if (oi < idx) {
-                    idx = oi;
-                    pos = op;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const uint32_t wexcl = incl - n_own;
+            const unsigned long long rs = run + n_g;  // output index of the slice's first integer
+            // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
+            uint32_t bad16 = 0;
+            if (Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3)) {
+                const uint32_t five = (Tx >> 3) & (Cx >> 4) & (Cx >> 5) & (Cx >> 6) & (Cx >> 7) & inr16;
+                if (five) {
+                    const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
+                    const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
+                    const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
+                    const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
+                    bad16 = five & hibits16(g0, g1, g2, g3);
                 }
             }
-            if (lane == 0) sink_error(K, idx, pos, limit);
-        }
-        if (n_w == 0) continue;  // warp-uniform
-        // end of integer limit-1, if it ends in this slice
-        if (limit - run <= n_w && limit - 1 - run >= wexcl && limit - 1 - run < wexcl + n_own) {
-            uint32_t m = ends16;
-            for (unsigned r = static_cast<unsigned>(limit - 1 - run - wexcl); r > 0; --r) m &= m - 1;
-            sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
-        }
-        if (wexcl + n_own == n_w && n_own) last_end = q0 + (31 - __clz(ends16)) + 1 - R.lo;
-
-        // ---- V digit windows (positions -8 .. 511 of the slice) and EP ends ----
-        const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3), dn = digits4(wn);
-        const uint32_t vo = 4u * r0;
-        *reinterpret_cast<uint4*>(vbase + v_swz(vo)) = vquad(d0, d1);
-        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 16)) = vquad(d1, d2);
-        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 32)) = vquad(d2, d3);
-        *reinterpret_cast<uint4*>(vbase + v_swz(vo + 48)) = vquad(d3, dn);
-        if (lane == 0) {
-            const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
-            *reinterpret_cast<uint4*>(vbase + v_swz(0)) = vquad(dp2, dp3);
-            *reinterpret_cast<uint4*>(vbase + v_swz(16)) = vquad(dp3, d0);
-            const uint32_t tp8 = Tx & 0xFFu;  // positions -8..-1 -> V index 0..7
-            // the range start is an integer boundary: the padding before it
-            // holds no integers (they are masked out of ends16)
-            eph[7] = (q <= R.lo) ? static_cast<uint16_t>(7 + (R.lo - q))
-                                 : static_cast<uint16_t>(tp8 ? 31 - __clz(tp8) : 0xFFFF);
-        }
-        uint16_t* ep = eph + 8 + wexcl;
+            if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the slice's first malformed integer
+                const int j = bad16 ? __ffs(bad16) - 1 : 0;
+                unsigned long long idx = bad16 ? rs + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
+                long long pos = q0 + j - 4 - R.lo;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if ((ends16 >> j) & 1u) {
-                *ep = static_cast<uint16_t>(r0 + j);
-                ++ep;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+                    const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
+                    if (oi < idx) {
+                        idx = oi;
+                        pos = op;
+                    }
+                }
+                if (lane == 0) sink_error(K, idx, pos, limit);
             }
-        }
-        if (n_own && wexcl + n_own == n_w) {  // zero-width padding for the last octet
-            const uint16_t rl = static_cast<uint16_t>(r0 + (31 - __clz(ends16)));
+            if (n_w == 0) continue;  // warp-uniform (the next slice writes its own halo V)
+            // end of integer limit-1, if it ends in this slice
+            if (limit - rs <= n_w && limit - 1 - rs >= wexcl && limit - 1 - rs < wexcl + n_own) {
+                uint32_t m = ends16;
+                for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
+                sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
+            }
+            if (wexcl + n_own == n_w && n_own) last_end = q0 + (31 - __clz(ends16)) + 1 - R.lo;
+
+            // ---- V digit windows and EP ends (V index = 8 + 512h + slice position) ----
+            const uint32_t rh = r0 + 512u * h;
+            const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3), dn = digits4(wn);
+            const uint32_t vo = 4u * rh;
+            *reinterpret_cast<uint4*>(vbase + v_swz(vo)) = vquad(d0, d1);
+            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 16)) = vquad(d1, d2);
+            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 32)) = vquad(d2, d3);
+            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 48)) = vquad(d3, dn);
+            if (lane == 0) {
+                const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
+                *reinterpret_cast<uint4*>(vbase + v_swz(2048u * h)) = vquad(dp2, dp3);
+                *reinterpret_cast<uint4*>(vbase + v_swz(2048u * h + 16)) = vquad(dp3, d0);
+                if (n_g == 0) {  // the group's first integer: its predecessor's end (V index)
+                    const uint32_t tp8 = Tx & 0xFFu;  // positions -8..-1
+                    // the range start is an integer boundary: the padding before it
+                    // holds no integers (they are masked out of ends16)
+                    eph[7] = (q <= R.lo) ? static_cast<uint16_t>(512u * h + 7 + (R.lo - q))
+                             : static_cast<uint16_t>(tp8 ? 512u * h + (31 - __clz(tp8)) : (512u * h - 1u) & 0xFFFFu);
+                }
+            }
+            uint16_t* ep = eph + 8 + n_g + wexcl;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) ep[k] = rl;
+            for (int j = 0; j < 16; ++j) {
+                if ((ends16 >> j) & 1u) {
+                    *ep = static_cast<uint16_t>(rh + j);
+                    ++ep;
+                }
+            }
+            if (n_own && wexcl + n_own == n_w) {  // zero-width padding for the last octet
+                const uint16_t rl = static_cast<uint16_t>(rh + (31 - __clz(ends16)));
+#pragma unroll
+                for (int k = 0; k < 8; ++k) ep[k] = rl;
+            }
+            n_g += n_w;
         }
+        if (n_g == 0) continue;
         __syncwarp();
 
         // ---- phase 2 and stores: 8 integers per lane per pass ----
-        for (uint32_t q2 = 0; q2 < n_w; q2 += 256) {
+        for (uint32_t q2 = 0; q2 < n_g; q2 += 256) {
             const uint32_t u = q2 + 8u * lane;
             uint32_t val[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) val[k] = 0;
-            if (u < n_w) {
+            if (u < n_g) {
                 const uint4 ea = *reinterpret_cast<const uint4*>(eph + 8 + u);  // 8 ends
                 const uint32_t e[9] = {eph[7 + u], ea.x & 0xFFFFu, ea.x >> 16, ea.y & 0xFFFFu, ea.y >> 16,
                                        ea.z & 0xFFFFu, ea.z >> 16, ea.w & 0xFFFFu, ea.w >> 16};
@@ -484,7 +500,7 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
             const unsigned long long gi = run + q2;  // output index of this pass's first integer
             if (gi < limit) {
                 const unsigned long long room = limit - gi;
-                const unsigned npass = n_w - q2 < 256u ? n_w - q2 : 256u;
+                const unsigned npass = n_g - q2 < 256u ? n_g - q2 : 256u;
                 const unsigned plim = room < npass ? static_cast<unsigned>(room) : npass;
                 uint32_t* const op = out + gi;
                 switch ((4u - static_cast<unsigned>((out_w + gi) & 3u)) & 3u) {
@@ -495,8 +511,8 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
                 }
             }
         }
-        run += n_w;
-        __syncwarp();  // V / EP are rewritten by the next slice
+        run += n_g;
+        __syncwarp();  // V / EP are rewritten by the next group
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
