@@ -136,6 +136,9 @@ constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + t
 // (head, at most 4: lane 0's halo word) and leaves out the bytes after its
 // last terminator (tail, at most 4 in canonical data: lane 31's last words).
 template <bool kDelta>
+__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane);
+
+template <bool kDelta>
 __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -143,7 +146,11 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const long long per = (S.n_seg + nw - 1) / nw;
     const long long s_begin = gw * per;
     const long long s_end = s_begin + per < S.n_seg ? s_begin + per : S.n_seg;
-    if (s_begin >= s_end) return;
+    if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane);
+}
+
+template <bool kDelta>
+__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane) {
     const long long its_per_seg = S.seg_bytes / kSegASlice;
     const long long q_begin = s_begin * S.seg_bytes, q_end = s_end * S.seg_bytes;
 
@@ -523,19 +530,380 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
     ro.n = run - base;
 }
 
+// ------------------------------------------------------------------ lane-local range decode
+
+// The same contract as decode_range, computed the other way round: every lane
+// decodes, in registers, the integers whose terminator lies in its own 16
+// bytes, and writes them in output order into a warp-private staging buffer;
+// the warp then copies the staging buffer out with 16-byte-aligned quads.
+//
+// Per lane: the 7-bit digits of its words are packed (pack28, 28 bits per
+// word) into 56-bit windows (word k-1, word k), so an integer ending at byte t
+// of word k is one funnel shift (its end to the top of a register) and one
+// shift right by 32 - 7 * length.  The lengths come from a chain over the
+// lane's 16 bytes (sh = 32 - 7 * length: 25 after a terminator, 7 less per
+// continuation byte), started from the terminators of the 4 bytes before.
+// Sixteen static slots, one per byte position; a slot stores iff its byte is
+// a terminator.
+//
+// A slice takes the fast path (lane_slots_fast) when it lies inside the
+// range, does not hold integer limit-1 and no lane sees four continuation
+// bytes in a row in its 4 bytes before and its own 16 (so every integer has
+// 1..4 bytes and none is malformed) -- a warp-uniform test; otherwise the
+// general path (ll_slice_gen: range masks, 5-byte integers, malformed
+// integers, the end of integer limit-1).  Delta: in-lane running sums stay in
+// registers, the warp scan of the lane totals adds the offsets before the
+// stores.
+#ifndef MVB_LL_BLOCKS
+#define MVB_LL_BLOCKS 6
+#endif
+constexpr int kLLBlocks = MVB_LL_BLOCKS;           // resident CTAs per SM the register budget targets
+constexpr int kLaneGroup = 2;                      // slices per staging copy-out
+constexpr int kLaneStage = kLaneGroup * 512 + 8;   // staging words per warp (+ alignment)
+constexpr int kLaneWarpBytes = 4 * kLaneStage + 1024;  // staging + 2 x 512-byte input ring
+constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
+static_assert((4 * kLaneStage) % 16 == 0, "staging alignment");
+
+// 7-bit digits of the four bytes of w, packed LSB first (28 bits).
+__device__ __forceinline__ uint32_t pack28(uint32_t w) {
+    const uint32_t d = w & 0x7F7F7F7Fu;
+    return __dp4a(d, 0x00008001u, 0u) + (__dp4a(d, 0x80010000u, 0u) << 14);
+}
+// x >> n with PTX semantics (n >= 32, or negative as unsigned, gives 0)
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, int n) {
+    uint32_t r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+    return r;
+}
+
 template <bool kDelta>
-__global__ void __launch_bounds__(kSegThreads, 8) vbyte_seg_decode(SegParams S) {
+__device__ __forceinline__ uint32_t lane_scan_offset(uint32_t total, uint32_t& carry) {
+    uint32_t xs = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xs, o);
+        if ((threadIdx.x & 31) >= o) xs += y;
+    }
+    const uint32_t ex = carry + xs - total;
+    carry += __shfl_sync(0xFFFFFFFFu, xs, 31);
+    return ex;
+}
+
+// Fast slots (see above): sp = shared-memory address of the lane's first
+// output.  Per slot e: p = byte e terminates; v = umulhi(top, m) with
+// m = 2^(7 * length) (the integer's bits are the top 7 * length bits of top);
+// next m = p ? 2^7 : m * 2^7.  The multiplies run on the FMA pipe, leaving the
+// (half-rate) ALU pipe the predicate, the selects and the funnel shift.
+template <bool kDelta>
+__device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                                uint32_t T16, uint32_t sp, uint32_t& carry) {
+    const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
+    const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
+    const uint32_t hi[4] = {c0 >> 4, c1 >> 4, c2 >> 4, c3 >> 4};
+    // length of the integer ending at byte 0 = 4 - (last terminator among bytes -4..-1)
+    uint32_t m = 1u << (28 - 7 * (31 - __clz(static_cast<int>(hibits4(~wp3)))));
+    if (kDelta) {
+        uint32_t val[16];
+        uint32_t prev = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const uint32_t top = __funnelshift_r(lo[e >> 2], hi[e >> 2], 3 + 7 * (e & 3));
+            uint32_t mn;
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\t"
+                "and.b32 t, %3, %5;\n\t"
+                "setp.ne.b32 p, t, 0;\n\t"
+                "mul.hi.u32 v, %4, %2;\n\t"
+                "selp.b32 v, v, 0, p;\n\t"
+                "add.u32 %0, %6, v;\n\t"
+                "mul.lo.u32 t, %2, 128;\n\t"
+                "selp.b32 %1, 128, t, p;\n\t"
+                "}"
+                : "=r"(val[e]), "=r"(mn)
+                : "r"(m), "r"(T16), "r"(top), "r"(1u << e), "r"(prev));
+            prev = val[e];
+            m = mn;
+        }
+        const uint32_t ex = lane_scan_offset<kDelta>(val[15], carry);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                         "and.b32 t, %1, %2;\n\t"
+                         "setp.ne.b32 p, t, 0;\n\t"
+                         "add.u32 t, %3, %4;\n\t"
+                         "@p st.shared.u32 [%0], t;\n\t"
+                         "@p add.u32 %0, %0, 4;\n\t"
+                         "}"
+                         : "+r"(sp)
+                         : "r"(T16), "r"(1u << e), "r"(val[e]), "r"(ex)
+                         : "memory");
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const uint32_t top = __funnelshift_r(lo[e >> 2], hi[e >> 2], 3 + 7 * (e & 3));
+            asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+                         "and.b32 t, %2, %4;\n\t"
+                         "setp.ne.b32 p, t, 0;\n\t"
+                         "mul.hi.u32 t, %3, %1;\n\t"
+                         "@p st.shared.u32 [%0], t;\n\t"
+                         "@p add.u32 %0, %0, 4;\n\t"
+                         "mul.lo.u32 t, %1, 128;\n\t"
+                         "selp.b32 %1, 128, t, p;\n\t"
+                         "}"
+                         : "+r"(sp), "+r"(m)
+                         : "r"(T16), "r"(top), "r"(1u << e)
+                         : "memory");
+        }
+    }
+}
+
+// General slots: integers of 1..5 bytes, terminators restricted to ends16
+// (bytes outside the range), malformed runs decode to garbage (their index
+// is reported by ll_slice_gen; nothing after it is meaningful).
+template <bool kDelta>
+__device__ __forceinline__ void lane_slots_gen(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                               uint32_t T16, uint32_t ends16, uint32_t* sp, uint32_t& carry) {
+    const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
+    const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
+    const uint32_t hi[4] = {c0 >> 4, c1 >> 4, c2 >> 4, c3 >> 4};
+    int sh = 7 * (31 - __clz(static_cast<int>(hibits4(~wp3)))) + 4;  // -3 if no terminator in the 4 bytes before
+    uint32_t val[16];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        if (e) sh = ((T16 >> (e - 1)) & 1u) ? 25 : sh - 7;
+        const int k = e >> 2, t = e & 3;
+        const uint32_t top = __funnelshift_r(lo[k], hi[k], 3 + 7 * t);  // packed bits ending with byte e
+        uint32_t v = shr_clamp(top, sh);
+        if (sh < 0) v = __funnelshift_r(lo[k], hi[k], 7 * t);  // five bytes: the low 32 bits
+        if (kDelta) {
+            if ((ends16 >> e) & 1u) acc += v;
+            val[e] = acc;
+        } else if ((ends16 >> e) & 1u) {
+            *sp++ = v;
+        }
+    }
+    if (kDelta) {
+        const uint32_t ex = lane_scan_offset<kDelta>(acc, carry);
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if ((ends16 >> e) & 1u) *sp++ = val[e] + ex;
+    }
+}
+
+// The general path of one slice (after the count scan): malformed integers,
+// the end of integer limit-1, then the general slots.
+template <bool kDelta>
+__device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
+                                          uint32_t w3, uint32_t wp3, uint32_t T16, uint32_t inr16, uint32_t n_own,
+                                          uint32_t n_w, uint32_t wexcl, unsigned long long rs,
+                                          unsigned long long limit, const RangeSink& K, uint32_t* sp,
+                                          uint32_t& carry) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ends16 = T16 & inr16;
+    uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1);
+    if (lane == 0) wp2 = r_inside(R, q0 - 8, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + q0 - 8))
+                                                : r_word(R, q0 - 8);
+    const uint32_t Tx = hibits4(~wp2) | (hibits4(~wp3) << 4) | (T16 << 8);  // positions -8..15
+    const uint32_t Cx = ~Tx & 0x00FFFFFFu;
+    const uint32_t run4 = Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3);
+    uint32_t bad16 = 0;
+    if (run4) {  // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
+        const uint32_t five = (Tx >> 3) & (run4 >> 4) & inr16;
+        if (five) {
+            const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
+            const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
+            const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
+            const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
+            bad16 = five & hibits16(g0, g1, g2, g3);
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the slice's first malformed integer
+        const int j = bad16 ? __ffs(bad16) - 1 : 0;
+        unsigned long long idx = bad16 ? rs + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
+        long long pos = q0 + j - 4 - R.lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+            const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
+            if (oi < idx) {
+                idx = oi;
+                pos = op;
+            }
+        }
+        if (lane == 0) sink_error(K, idx, pos, limit);
+    }
+    if (n_w == 0) return;
+    // end of integer limit-1, if it ends in this slice
+    if (limit - rs <= n_w && limit - 1 - rs >= wexcl && limit - 1 - rs < wexcl + n_own) {
+        uint32_t m = ends16;
+        for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
+        sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
+    }
+    lane_slots_gen<kDelta>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
+}
+
+// Copy stage[a, a + n) to out[run, run + n), indices below `limit` only;
+// stage[i] <-> out[run - a + i] with out + run - a 16-byte aligned.  Whole
+// quads in the loop; the partial first quad [a, 4) and last quad
+// [end & ~3, end) by lanes 0..3 and 4..7, one integer each.
+__device__ __forceinline__ void stage_out(const uint32_t* stage, uint32_t a, uint32_t n, unsigned long long run,
+                                          unsigned long long limit, uint32_t* out, int lane) {
+    if (run >= limit) return;
+    const unsigned long long g0 = run - a;
+    const unsigned long long room = limit - g0;
+    const uint32_t end = (static_cast<unsigned long long>(a + n) < room) ? a + n : static_cast<uint32_t>(room);
+    uint32_t* const ob = out + g0;
+    const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
+    if (lane < 8) {
+        const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) ob[i] = stage[i];
+    }
+    for (uint32_t i = i0 + 4 * lane; i < i1; i += 128)
+        *reinterpret_cast<uint4*>(ob + i) = *reinterpret_cast<const uint4*>(stage + i);
+}
+
+// cp.async prefetch of the next slice into a warp's 2 x 512-byte ring
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ring: shared-memory address of the warp's 2 x 512-byte input ring.  Slices
+// are indexed from qs; interior slices (inside [R.lo, R.hi)) arrive by
+// cp.async one slice ahead into ring half (i & 1), the others are read with
+// range masks.
+template <bool kDelta>
+__device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs, long long qe,
+                                                unsigned long long base, uint32_t carry, unsigned long long limit,
+                                                uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
+                                                const RangeSink& K, RangeOut& ro) {
+    const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
+    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const int ns = static_cast<int>((qe - qs + kSegSlice - 1) / kSegSlice);
+    int i_lo, i_hi;  // interior slices: i_lo <= i < i_hi
+    {
+        const long long d = R.lo - qs, e = R.hi - qs;
+        const long long lo = d <= 0 ? 0 : (d + kSegSlice - 1) / kSegSlice;
+        const long long hi = e <= 0 ? 0 : e / kSegSlice;
+        i_lo = static_cast<int>(lo < ns ? lo : ns);
+        i_hi = static_cast<int>(hi < ns ? hi : ns);
+    }
+    const uint8_t* const pin = R.ab + qs + 16 * lane;  // this lane's bytes of slice 0
+    const uint32_t rbase = ring + 16u * lane;
+    // integers that may still be stored before `limit` (clamped): a slice with fewer takes the fast path
+    uint32_t left;
+    {
+        const unsigned long long r = limit > base ? limit - base : 0ull;
+        left = r > 0x7FFFFFFFull ? 0x7FFFFFFFu : static_cast<uint32_t>(r);
+    }
+    unsigned long long run = base;  // output index of the group's first integer
+    int last_i = -1;                // the last slice holding an integer (warp-uniform)
+    uint32_t pw3 = 0;               // lane 0: the 4 bytes before the slice
+    if (lane == 0) pw3 = r_inside(R, qs - 4, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + qs - 4))
+                                                : r_word(R, qs - 4);
+    if (i_lo == 0 && i_hi > 0) {
+        cp_async16(rbase, pin);
+        cp_async_commit();
+    }
+    for (int g = 0; g < ns; g += kLaneGroup) {
+        const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the group
+        uint32_t n_g = 0;
+#pragma unroll 1
+        for (int i = g; i < g + kLaneGroup && i < ns; ++i) {
+            const bool inter = i >= i_lo && i < i_hi;  // warp-uniform
+            const bool pfn = i + 1 >= i_lo && i + 1 < i_hi;
+            if (pfn) {
+                cp_async16(rbase + 512u * ((i + 1) & 1), pin + kSegSlice * (i + 1));
+                cp_async_commit();
+            }
+            uint4 x;
+            if (inter) {
+                if (pfn) cp_async_wait<1>();
+                else cp_async_wait<0>();
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                             : "r"(rbase + 512u * (i & 1))
+                             : "memory");
+            } else {
+                x = r_load16(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane);
+            }
+            const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
+            uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
+            const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
+            if (lane == 0) wp3 = pw3;
+            pw3 = l3;
+            const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
+            const uint32_t inr16 =
+                inter ? 0xFFFFu : r_inr16(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane);
+            const uint32_t n_own = __popc(T16 & inr16);
+            uint32_t incl = n_own;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const uint32_t wexcl = incl - n_own;
+            const uint32_t C20 = ~(hibits4(~wp3) | (T16 << 4)) & 0xFFFFFu;  // continuation bytes, positions -4..15
+            const uint32_t run4 = C20 & (C20 >> 1) & (C20 >> 2) & (C20 >> 3);
+            const bool fast = !__any_sync(0xFFFFFFFFu, run4) && inter && n_w < left;
+            if (n_w) last_i = i;
+            if (fast)
+                lane_slots_fast<kDelta>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
+            else
+                ll_slice_gen<kDelta>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3, wp3,
+                                     T16, inr16, n_own, n_w, wexcl, run + n_g, limit, K, stage + a + n_g + wexcl,
+                                     carry);
+            n_g += n_w;
+            left = left > n_w ? left - n_w : 0u;
+        }
+        if (n_g == 0) continue;
+        __syncwarp();
+        stage_out(stage, a, n_g, run, limit, out, lane);
+        run += n_g;
+        __syncwarp();  // the staging buffer is rewritten by the next group
+    }
+    // the end of the range's last integer: in slice last_i
+    long long last_end = -1;
+    if (last_i >= 0) {
+        const long long q0 = qs + static_cast<long long>(kSegSlice) * last_i + 16 * lane;
+        const uint4 x = r_load16(R, q0);
+        const uint32_t e16 = hibits16(~x.x, ~x.y, ~x.z, ~x.w) & r_inr16(R, q0);
+        if (e16) last_end = q0 + (31 - __clz(e16)) + 1 - R.lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long le = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
+            last_end = le > last_end ? le : last_end;
+        }
+    }
+    ro.last_end = last_end;
+    ro.n = run - base;
+}
+
+// kLL: 0 decode_range (V / EP windows), 1 decode_range_ll (lane-local)
+template <bool kDelta, int kLL>
+__global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_decode(SegParams S) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    char* const vbase = reinterpret_cast<char*>(smem) + wid * (4 * kSegVW);
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
     uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
+    // kLL: one contiguous run of segments per warp (the output index and carry
+    // after segment s are those of s + 1, so only the run's first segment needs
+    // the prefix); otherwise segments round-robin.
+    const long long per = kLL ? (S.n_seg + nw - 1) / nw : 1;
+    const long long s0 = kLL ? gw * per : gw, s_step = kLL ? S.n_seg : nw;
 
-    for (long long s = gw; s < S.n_seg; s += nw) {
+    for (long long s = s0; s < S.n_seg; s += s_step) {
+        const long long s_end = kLL ? (s + per < S.n_seg ? s + per : S.n_seg) : s + 1;
         // ---- output index and carry of the segment: groups before + segments before in the group ----
         unsigned long long base = 0;
         unsigned long long csum = 0;
@@ -557,8 +925,12 @@ __global__ void __launch_bounds__(kSegThreads, 8) vbyte_seg_decode(SegParams S) 
         const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
         RangeOut ro;
         const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
-        decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph, lane,
-                             K, ro);
+        if (kLL)
+            decode_range_ll<kDelta>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                                    reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+        else
+            decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
+                                 lane, K, ro);
         if (lane == 0 && ro.last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
     }
 
@@ -641,7 +1013,7 @@ struct ListParams {
     WsHeader* hdr;
 };
 
-template <bool kDelta>
+template <bool kDelta, int kLL>
 __global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
@@ -649,8 +1021,9 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) 
     __shared__ long long s_err_pos[kSegWarps], s_count_end[kSegWarps];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    char* const vbase = reinterpret_cast<char*>(smem) + wid * (4 * kSegVW);
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
     uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
     while (true) {
         long long k = 0;
         if (lane == 0) k = static_cast<long long>(atomicAdd(&L.hdr->ticket, 1ull));
@@ -677,8 +1050,12 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) 
             __syncwarp();
             RangeOut ro;
             const RangeSink K = {nullptr, &s_err_idx[wid], &s_err_pos[wid], &s_count_end[wid]};
-            decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, kDelta && L.prev ? L.prev[l] : 0u, base + cnt, L.out,
-                                 vbase, eph, lane, K, ro);
+            const uint32_t carry = kDelta && L.prev ? L.prev[l] : 0u;
+            if (kLL)
+                decode_range_ll<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
+                                        reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+            else
+                decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out, vbase, eph, lane, K, ro);
             __syncwarp();
             const unsigned long long ei = s_err_idx[wid];
             if (ei != ~0ull && ei < base + cnt) {

@@ -75,9 +75,11 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
-// Strict-mode kernel: 0 segmented two-kernel decode (default, decode_seg.cuh), 1 per-tile
-// kernel, 2 warp-tile kernel, 3 warp-sliced v3 (decode_v3.cuh), 4 CTA-pipelined single pass
-// (decode_pipelined.cuh; also the traced kernel).
+// Strict-mode kernel: 0 segmented two-kernel decode with the lane-local range
+// decode (default, decode_seg.cuh: decode_range_ll), 1 per-tile kernel, 2
+// warp-tile kernel, 3 warp-sliced v3 (decode_v3.cuh), 4 CTA-pipelined single
+// pass (decode_pipelined.cuh; also the traced kernel), 5 segmented with the
+// V/EP-window range decode (decode_range).  Batched lists follow 0 / 5.
 // Permissive mode always runs the per-tile kernel (it needs a third lookback
 // component inside phase 1).  The switch exists for profiling comparisons.
 int g_kernel_choice = 0;
@@ -118,20 +120,21 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
 
 // Two-kernel segmented strict decode (decode_seg.cuh): group accumulators
 // zeroed, segment totals, then one warp per segment.
-template <bool Delta>
+template <bool Delta, int LL>
 int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
     static int per_sm = -1;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return MVB_ERR_CUDA;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return MVB_ERR_CUDA;
     if (per_sm < 0) {
-        if (cudaFuncSetAttribute(mvbk::vbyte_seg_decode<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kSegSmem) != cudaSuccess)
+        if (cudaFuncSetAttribute(mvbk::vbyte_seg_decode<Delta, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_decode<Delta>, mvbk::kSegThreads,
-                                                          mvbk::kSegSmem) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_decode<Delta, LL>, mvbk::kSegThreads,
+                                                          kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         per_sm = n > 0 ? n : 1;
     }
@@ -179,7 +182,7 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, 0, s>>>(S);
     const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
     const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
-    mvbk::vbyte_seg_decode<Delta><<<grid_b, mvbk::kSegThreads, mvbk::kSegSmem, s>>>(S);
+    mvbk::vbyte_seg_decode<Delta, LL><<<grid_b, mvbk::kSegThreads, kSmemB, s>>>(S);
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
@@ -288,7 +291,9 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.trace = trace;
 
     if (mode == MVB_STRICT && g_kernel_choice == 0 && trace == nullptr)
-        return delta ? launch_seg<true>(p, ws, ws_bytes, stream) : launch_seg<false>(p, ws, ws_bytes, stream);
+        return delta ? launch_seg<true, 1>(p, ws, ws_bytes, stream) : launch_seg<false, 1>(p, ws, ws_bytes, stream);
+    if (mode == MVB_STRICT && g_kernel_choice == 5 && trace == nullptr)
+        return delta ? launch_seg<true, 0>(p, ws, ws_bytes, stream) : launch_seg<false, 0>(p, ws, ws_bytes, stream);
     {
         const unsigned long long family = warp_kernel ? 2 : v3_kernel ? 3 : 1;
         const unsigned long long units = warp_kernel ? wtiles : tiles;
@@ -455,8 +460,8 @@ int mvb_shard_carry_device(const unsigned long long* records, int n_ranks, int r
 }  // extern "C"
 
 namespace {
-template <bool Delta>
-int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+template <bool Delta, int LL>
+int lists_device_t(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
                  const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, const unsigned* order,
                  uint32_t* out, int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n_lists == 0) return 0;
@@ -464,18 +469,19 @@ int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byt
     if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;  // permissive lists: decode each list on its own
     if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
+    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
     static int per_sm = -1;
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         return MVB_ERR_CUDA;
     if (per_sm < 0) {
-        if (cudaFuncSetAttribute(mvbk::vbyte_lists_decode<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kSegSmem) != cudaSuccess)
+        if (cudaFuncSetAttribute(mvbk::vbyte_lists_decode<Delta, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_lists_decode<Delta>, mvbk::kSegThreads,
-                                                          mvbk::kSegSmem) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_lists_decode<Delta, LL>, mvbk::kSegThreads,
+                                                          kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         per_sm = n > 0 ? n : 1;
     }
@@ -495,8 +501,18 @@ int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byt
     const long long warps_needed = static_cast<long long>(n_lists);
     const long long ctas = std::min<long long>(static_cast<long long>(per_sm) * sms,
                                                (warps_needed + mvbk::kSegWarps - 1) / mvbk::kSegWarps);
-    mvbk::vbyte_lists_decode<Delta><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, mvbk::kSegSmem, s>>>(L);
+    mvbk::vbyte_lists_decode<Delta, LL><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+template <bool Delta>
+int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                 const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, const unsigned* order,
+                 uint32_t* out, int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
+    return g_kernel_choice == 5
+               ? lists_device_t<Delta, 0>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev,
+                                          ws, ws_bytes, s)
+               : lists_device_t<Delta, 1>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev,
+                                          ws, ws_bytes, s);
 }
 }  // namespace
 
@@ -634,7 +650,9 @@ void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
 // Kernels one decode call launches in steady state (bench accounting; the
 // workspace re-zeroing memset runs only when a workspace changes layout).
-int mvbx_kernels_per_decode(int mode) { return (mode == MVB_STRICT && g_kernel_choice == 0) ? 2 : 1; }
+int mvbx_kernels_per_decode(int mode) {
+    return (mode == MVB_STRICT && (g_kernel_choice == 0 || g_kernel_choice == 5)) ? 2 : 1;
+}
 
 const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }
 

@@ -283,7 +283,7 @@ def test_config4_full_size_device(golden, oracle, cuda):
     assert oracle.fnv_u32(got) == s["out_fnv"]
 
 
-@pytest.mark.parametrize("choice", [1, 2, 3, 4, 0])
+@pytest.mark.parametrize("choice", [1, 2, 3, 4, 5, 0])
 def test_every_strict_kernel_variant(choice, golden, oracle):
     """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined, warp-sliced) agree with
     the oracle on KATs, errors across tile boundaries and a full config."""
@@ -338,7 +338,7 @@ def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
         v = W.mixed_values(n, seed)
         streams.append((v, oracle.encode_sequence(v)))
     try:
-        for choice in (0, 4, 1, 3, 2, 0):
+        for choice in (0, 4, 1, 3, 2, 5, 0):
             _lib.set_kernel_choice(choice)
             for rep in range(2):
                 for (v, enc), mode in zip(streams * 2, [STRICT] * 5 + [PERMISSIVE] * 5):
@@ -353,8 +353,9 @@ def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
         _lib.set_kernel_choice(0)
 
 
+@pytest.mark.parametrize("choice", [0, 5])
 @pytest.mark.parametrize("delta", [True, False])
-def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta):
+def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta, choice):
     """mvb_decode[_delta]_lists_device against one oracle decode per list,
     including empty lists, count-limited lists (more bytes than integers),
     truncated and malformed lists, unaligned list starts and a longest-first
@@ -388,10 +389,17 @@ def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta):
     out = torch.full((int(int_off[-1]) + 4,), -1, dtype=torch.int32, device=cuda)
     res = torch.zeros(len(parts) * 3, dtype=torch.int64, device=cuda)
     order = np.argsort(-np.diff(byte_off).astype(np.int64), kind="stable").astype(np.uint32)
+    from paper_1503_07387_b200 import _lib
+
     d = mvb.Decoder(cuda, 1 << 16)
-    d.decode_lists(src, torch.from_numpy(byte_off.view(np.int64)).to(cuda), torch.from_numpy(int_off.view(np.int64)).to(cuda),
-                   out, prev=torch.from_numpy(np.array(prevs, np.uint32).view(np.int32)).to(cuda) if delta else None,
-                   order=torch.from_numpy(order.view(np.int32)).to(cuda), results=res, delta=delta)
+    _lib.set_kernel_choice(choice)
+    try:
+        d.decode_lists(src, torch.from_numpy(byte_off.view(np.int64)).to(cuda),
+                       torch.from_numpy(int_off.view(np.int64)).to(cuda), out,
+                       prev=torch.from_numpy(np.array(prevs, np.uint32).view(np.int32)).to(cuda) if delta else None,
+                       order=torch.from_numpy(order.view(np.int32)).to(cuda), results=res, delta=delta)
+    finally:
+        _lib.set_kernel_choice(0)
     got = out.cpu().numpy().view(np.uint32)
     rr = res.cpu().numpy().reshape(-1, 3)
     for l, e in enumerate(parts):
