@@ -149,10 +149,56 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane);
 }
 
+// Digit-weight sums of a lane's words: weight 1 after a terminator, 128
+// after one continuation byte -- one funnel shift (the previous byte's high
+// bit to bit 0 of each byte) and one IMAD per word, then a dp4a.  Bytes
+// after two or more continuation bytes (integers of 3..5 bytes, rare in
+// delta-coded lists) also get 128 here; a second pass, taken when any lane of
+// the warp has one, corrects them to 2^14 / 2^21 / 2^28.
+template <int kW>
+__device__ __forceinline__ uint32_t words_digit_sum(const uint32_t (&w)[kW], uint32_t& hi) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 2; k < kW; ++k) {
+        const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u;
+        const uint32_t c1b = __funnelshift_l(cp, ck, 1);  // bit 0 of byte j: byte j-1 continues
+        hi |= c1b & __funnelshift_l(cp, ck, 9);          // ... and byte j-2 too
+        sum = __dp4a(w[k] & 0x7F7F7F7Fu, c1b * 127u + 0x01010101u, sum);
+    }
+    return sum;
+}
+template <int kW>
+__device__ __forceinline__ uint32_t words_digit_sum_hi(const uint32_t (&w)[kW]) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 2; k < kW; ++k) {
+        const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u, cpp = w[k - 2] & 0x80808080u;
+        const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+        const uint32_t c3 = __funnelshift_l(cp, ck, 24), c4 = cp;
+        const uint32_t c5 = __funnelshift_l(cpp, cp, 8);
+        const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
+        sum += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3 & ~c4), 0u) << 14;
+        sum += __dp4a(b, (cc & c3 & c4 & ~c5) >> 7, 0u) << 28;
+        sum -= __dp4a(b, cc >> 7, 0u) << 7;  // the weight 128 the first pass gave them
+    }
+    return sum;
+}
+
 template <bool kDelta>
 __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane) {
-    const long long its_per_seg = S.seg_bytes / kSegASlice;
+    const int its_per_seg = static_cast<int>(S.seg_bytes / kSegASlice);
     const long long q_begin = s_begin * S.seg_bytes, q_end = s_end * S.seg_bytes;
+    const int n_it = static_cast<int>((q_end - q_begin) / kSegASlice);
+    int i_lo, i_hi;  // iterations whose kSegASlice bytes all lie inside the stream: i_lo <= it < i_hi
+    {
+        const long long d = S.mis - q_begin, e = S.mis + S.len - q_begin;
+        const long long lo = d <= 0 ? 0 : (d + kSegASlice - 1) / kSegASlice;
+        const long long hi = e <= 0 ? 0 : e / kSegASlice;
+        i_lo = static_cast<int>(lo < n_it ? lo : n_it);
+        i_hi = static_cast<int>(hi < n_it ? hi : n_it);
+    }
+    constexpr int L = 16 * kSegAChunks;  // bytes per lane per iteration
+    const uint8_t* const pin = S.in - S.mis + q_begin + L * lane;
 
     uint32_t pw2 = 0, pw3 = 0;  // the 8 bytes before the current iteration (for lane 0)
     if (lane == 0) {
@@ -165,15 +211,15 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             pw3 = seg_word(S, q_begin - 4);
         }
     }
-    constexpr int L = 16 * kSegAChunks;  // bytes per lane per iteration
     uint4 nx[kSegAChunks];
 #pragma unroll
-    for (int c = 0; c < kSegAChunks; ++c) nx[c] = seg_load16(S, q_begin + L * lane + 16 * c);
+    for (int c = 0; c < kSegAChunks; ++c)
+        nx[c] = (0 >= i_lo && 0 < i_hi) ? ldg_stream16(pin + 16 * c) : seg_load16(S, q_begin + L * lane + 16 * c);
     unsigned cnt = 0;
     uint32_t sum = 0;
     long long s = s_begin;
-    long long it = 0;  // iteration within segment s
-    for (long long q = q_begin; q < q_end; q += kSegASlice) {
+    int it_s = 0;  // iteration within segment s
+    for (int it = 0; it < n_it; ++it) {
         uint32_t w[kSegAW];  // w[0], w[1]: the 8 bytes before this lane's bytes; then the lane's words
 #pragma unroll
         for (int c = 0; c < kSegAChunks; ++c) {
@@ -182,9 +228,14 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             w[4 + 4 * c] = nx[c].z;
             w[5 + 4 * c] = nx[c].w;
         }
-        if (q + kSegASlice < q_end) {
+        const bool inter = it >= i_lo && it < i_hi;
+        if (it + 1 < n_it) {
+            const bool inter_n = it + 1 >= i_lo && it + 1 < i_hi;
 #pragma unroll
-            for (int c = 0; c < kSegAChunks; ++c) nx[c] = seg_load16(S, q + kSegASlice + L * lane + 16 * c);
+            for (int c = 0; c < kSegAChunks; ++c)
+                nx[c] = inter_n ? ldg_stream16(pin + static_cast<long long>(kSegASlice) * (it + 1) + 16 * c)
+                                : seg_load16(S, q_begin + static_cast<long long>(kSegASlice) * (it + 1) + L * lane +
+                                                    16 * c);
         }
         w[0] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 2], 1);
         w[1] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 1], 1);
@@ -195,15 +246,14 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         }
         pw2 = l2;
         pw3 = l3;
-        const bool seg_first = it == 0, seg_last = it == its_per_seg - 1;
-        const long long ql = q + L * lane;
-        const bool edge = !seg_inside(S, ql, L);  // stream start / end inside these bytes
-        if (!edge) {
+        const bool seg_first = it_s == 0, seg_last = it_s == its_per_seg - 1;
+        if (inter) {
             unsigned nc = 0;
 #pragma unroll
             for (int k = 2; k < kSegAW; ++k) nc += __popc(w[k] & 0x80808080u);
             cnt += L - nc;
         } else {
+            const long long ql = q_begin + static_cast<long long>(kSegASlice) * it + L * lane;
 #pragma unroll
             for (int c = 0; c < kSegAChunks; ++c) {
                 const uint32_t T16 = hibits16(~w[2 + 4 * c], ~w[3 + 4 * c], ~w[4 + 4 * c], ~w[5 + 4 * c]);
@@ -211,28 +261,9 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             }
         }
         if (kDelta) {
-            // classes 0/1 for every word (weights 1 / 128 per byte, one dp4a each)
-            uint32_t hiacc = 0;
-#pragma unroll
-            for (int k = 2; k < kSegAW; ++k) {
-                const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u;
-                const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
-                hiacc |= c1 & c2;
-                sum = __dp4a(w[k] & 0x7F7F7F7Fu, ((c1 >> 7) ^ 0x01010101u) | (c1 & ~c2), sum);
-            }
-            if (__any_sync(0xFFFFFFFFu, hiacc)) {
-                // integers of 3..5 bytes somewhere in the warp: classes 2..4
-#pragma unroll
-                for (int k = 2; k < kSegAW; ++k) {
-                    const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u, cpp = w[k - 2] & 0x80808080u;
-                    const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
-                    const uint32_t c3 = __funnelshift_l(cp, ck, 24), c4 = cp;
-                    const uint32_t c5 = __funnelshift_l(cpp, cp, 8);
-                    const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
-                    sum += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3 & ~c4), 0u) << 14;
-                    sum += __dp4a(b, (cc & c3 & c4 & ~c5) >> 7, 0u) << 28;
-                }
-            }
+            uint32_t hi = 0;
+            sum += words_digit_sum(w, hi);
+            if (__any_sync(0xFFFFFFFFu, hi)) sum += words_digit_sum_hi(w);  // integers of 3..5 bytes
             if (seg_first && lane == 0) {
                 // head: bytes -4..-1 of the first integer ending in the segment
                 sum += word_digit_sum(w[1], w[0], 0u, after_last_terminator(w[1]), true);
@@ -263,9 +294,9 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             cnt = 0;
             sum = 0;
             ++s;
-            it = 0;
+            it_s = 0;
         } else {
-            ++it;
+            ++it_s;
         }
     }
 }
@@ -899,11 +930,11 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_de
     // kLL: one contiguous run of segments per warp (the output index and carry
     // after segment s are those of s + 1, so only the run's first segment needs
     // the prefix); otherwise segments round-robin.
-    const long long per = kLL ? (S.n_seg + nw - 1) / nw : 1;
-    const long long s0 = kLL ? gw * per : gw, s_step = kLL ? S.n_seg : nw;
+    const long long s0 = kLL ? gw * S.n_seg / nw : gw, s_step = kLL ? S.n_seg : nw;
+    const long long s0_end = kLL ? (gw + 1) * S.n_seg / nw : 0;  // balanced runs: sizes differ by at most one
 
-    for (long long s = s0; s < S.n_seg; s += s_step) {
-        const long long s_end = kLL ? (s + per < S.n_seg ? s + per : S.n_seg) : s + 1;
+    for (long long s = s0; s < (kLL ? s0_end : S.n_seg); s += s_step) {
+        const long long s_end = kLL ? s0_end : s + 1;
         // ---- output index and carry of the segment: groups before + segments before in the group ----
         unsigned long long base = 0;
         unsigned long long csum = 0;
