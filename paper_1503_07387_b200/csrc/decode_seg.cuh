@@ -5,8 +5,11 @@
 // equal segments of a multiple of 512 bytes, about four per resident warp.
 //
 //   A. vbyte_seg_totals: one warp per segment counts the integers that END
-//      in it (terminator bytes) and sums their values mod 2^32 (the totals
-//      pre-pass of the sharded decode, totals_kernel.cuh), and rolls both up
+//      in it (terminator bytes) and sums the digit weights of its bytes
+//      (digit * 128^(position in its integer), mod 2^32; the sums of the
+//      segments before a segment are the value sum of the integers before it
+//      plus the partial value of the integer straddling its start, which
+//      kernel B subtracts), and rolls both up
 //      into per-group (32 segments) accumulators (zero between launches:
 //      the finalizing CTA of kernel B re-zeroes them).  It reads the input once;
 //      for the SURVEY configs c1/c2/c5 the input then sits in the 126 MB L2
@@ -143,9 +146,7 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const long long per = (S.n_seg + nw - 1) / nw;
-    const long long s_begin = gw * per;
-    const long long s_end = s_begin + per < S.n_seg ? s_begin + per : S.n_seg;
+    const long long s_begin = gw * S.n_seg / nw, s_end = (gw + 1) * S.n_seg / nw;  // balanced runs
     if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane);
 }
 
@@ -246,7 +247,7 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         }
         pw2 = l2;
         pw3 = l3;
-        const bool seg_first = it_s == 0, seg_last = it_s == its_per_seg - 1;
+        const bool seg_last = it_s == its_per_seg - 1;
         if (inter) {
             unsigned nc = 0;
 #pragma unroll
@@ -264,17 +265,6 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             uint32_t hi = 0;
             sum += words_digit_sum(w, hi);
             if (__any_sync(0xFFFFFFFFu, hi)) sum += words_digit_sum_hi(w);  // integers of 3..5 bytes
-            if (seg_first && lane == 0) {
-                // head: bytes -4..-1 of the first integer ending in the segment
-                sum += word_digit_sum(w[1], w[0], 0u, after_last_terminator(w[1]), true);
-            }
-            if (seg_last && lane == 31) {
-                // tail: bytes after the segment's last terminator (in the last two words)
-                const uint32_t a1 = after_last_terminator(w[kSegAW - 1]);
-                const uint32_t a0 = (~w[kSegAW - 1] & 0x80808080u) ? 0u : after_last_terminator(w[kSegAW - 2]);
-                sum -= word_digit_sum(w[kSegAW - 1], w[kSegAW - 2], w[kSegAW - 3], a1, true) +
-                       word_digit_sum(w[kSegAW - 2], w[kSegAW - 3], w[kSegAW - 4], a0, true);
-            }
         }
         if (seg_last) {
             const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
@@ -634,38 +624,48 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint3
     // length of the integer ending at byte 0 = 4 - (last terminator among bytes -4..-1)
     uint32_t m = 1u << (28 - 7 * (31 - __clz(static_cast<int>(hibits4(~wp3)))));
     if (kDelta) {
-        uint32_t val[16];
-        uint32_t prev = 0;
+        // the lane's exclusive prefix up front: digit-weight sum of its 16 bytes,
+        // minus its tail (bytes after its last terminator: c3 >> 7 * (t + 1)), plus
+        // its head (the same for the 4 bytes before: the previous lane's tail)
+        const uint32_t tpl = 31 - __clz(static_cast<int>(hibits4(~wp3)));
+        const uint32_t t3 = 31 - __clz(static_cast<int>(T16 >> 12));
+        const uint32_t wd[5] = {wp3, w0, w1, w2, w3};
+        uint32_t S = 0, hic = 0;
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+            const uint32_t ck = wd[k] & 0x80808080u, cp = wd[k - 1] & 0x80808080u;
+            const uint32_t c1b = __funnelshift_l(cp, ck, 1);
+            hic |= c1b & __funnelshift_l(cp, ck, 9);
+            S = __dp4a(wd[k] & 0x7F7F7F7Fu, c1b * 127u + 0x01010101u, S);
+        }
+        if (__any_sync(0xFFFFFFFFu, hic)) {  // bytes after 2 or 3 continuation bytes: 2^14 / 2^21, not 128
+#pragma unroll
+            for (int k = 1; k < 5; ++k) {
+                const uint32_t ck = wd[k] & 0x80808080u, cp = wd[k - 1] & 0x80808080u;
+                const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+                const uint32_t c3 = __funnelshift_l(cp, ck, 24);
+                const uint32_t cc = c1 & c2, b = wd[k] & 0x7F7F7F7Fu;
+                S += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3), 0u) << 14;
+                S -= __dp4a(b, cc >> 7, 0u) << 7;
+            }
+        }
+        const uint32_t own = S - shr_clamp(c3, 7 * (t3 + 1)) + shr_clamp(cm, 7 * (tpl + 1));
+        uint32_t acc = lane_scan_offset<kDelta>(own, carry);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const uint32_t top = __funnelshift_r(lo[e >> 2], hi[e >> 2], 3 + 7 * (e & 3));
-            uint32_t mn;
-            asm("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\t"
-                "and.b32 t, %3, %5;\n\t"
-                "setp.ne.b32 p, t, 0;\n\t"
-                "mul.hi.u32 v, %4, %2;\n\t"
-                "selp.b32 v, v, 0, p;\n\t"
-                "add.u32 %0, %6, v;\n\t"
-                "mul.lo.u32 t, %2, 128;\n\t"
-                "selp.b32 %1, 128, t, p;\n\t"
-                "}"
-                : "=r"(val[e]), "=r"(mn)
-                : "r"(m), "r"(T16), "r"(top), "r"(1u << e), "r"(prev));
-            prev = val[e];
-            m = mn;
-        }
-        const uint32_t ex = lane_scan_offset<kDelta>(val[15], carry);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
             asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-                         "and.b32 t, %1, %2;\n\t"
+                         "and.b32 t, %3, %5;\n\t"
                          "setp.ne.b32 p, t, 0;\n\t"
-                         "add.u32 t, %3, %4;\n\t"
-                         "@p st.shared.u32 [%0], t;\n\t"
+                         "mul.hi.u32 t, %4, %2;\n\t"
+                         "@p add.u32 %1, %1, t;\n\t"
+                         "@p st.shared.u32 [%0], %1;\n\t"
                          "@p add.u32 %0, %0, 4;\n\t"
+                         "mul.lo.u32 t, %2, 128;\n\t"
+                         "selp.b32 %2, 128, t, p;\n\t"
                          "}"
-                         : "+r"(sp)
-                         : "r"(T16), "r"(1u << e), "r"(val[e]), "r"(ex)
+                         : "+r"(sp), "+r"(acc), "+r"(m)
+                         : "r"(T16), "r"(top), "r"(1u << e)
                          : "memory");
         }
     } else {
@@ -953,7 +953,17 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_de
             if (kDelta) csum += __shfl_xor_sync(0xFFFFFFFFu, csum, o);
         }
         if (base >= S.count) continue;  // nothing of this segment is stored (warp-uniform)
-        const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
+        // segment sums are digit-weight sums of the segments' bytes: the bytes before
+        // this segment that belong to the integer straddling its start (the partial
+        // value of the <= 4 bytes after the last terminator before it) are not yet
+        // an integer of the prefix
+        uint32_t straddle = 0;
+        if (kDelta) {
+            const uint32_t wb = r_word(R, s * S.seg_bytes - 4);
+            straddle = shr_clamp(pack28(wb), 7 * (32 - __clz(static_cast<int>(hibits4(~wb)))));
+        }
+        const uint32_t carry =
+            kDelta ? static_cast<uint32_t>(csum) - straddle + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
         RangeOut ro;
         const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
         if (kLL)

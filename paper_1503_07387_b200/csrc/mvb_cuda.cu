@@ -142,9 +142,8 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     const long long warps = ctas * mvbk::kSegWarps;
     const long long qlen = p.mis + p.len;
     // segments per kernel-B warp: LL decodes a balanced contiguous run of them per
-    // warp (finer is better balanced; delta pays a head/tail correction per
-    // segment in kernel A, so 4 there), V/EP hands them out round-robin
-    const long long per_warp = (LL && !Delta) ? 8 : 4;
+    // warp (finer is better balanced), V/EP hands them out round-robin
+    const long long per_warp = LL ? 8 : 4;
     long long seg = (qlen + per_warp * warps - 1) / (per_warp * warps);
     seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: 2 KiB slices
     if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
