@@ -580,10 +580,27 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 #endif
 constexpr int kLLBlocks = MVB_LL_BLOCKS;           // resident CTAs per SM the register budget targets
 constexpr int kLaneGroup = 2;                      // slices per staging copy-out
-constexpr int kLaneStage = kLaneGroup * 512 + 8;   // staging words per warp (+ alignment)
+constexpr int kLaneStage = kLaneGroup * 512 + 32;  // staging words per warp (+ alignment), whole 128-byte rows
 constexpr int kLaneWarpBytes = 4 * kLaneStage + 1024;  // staging + 2 x 512-byte input ring
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
-static_assert((4 * kLaneStage) % 16 == 0, "staging alignment");
+static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
+
+// Dense ranges (>= 7/8 integer per byte, i.e. mostly 1-byte integers) swizzle
+// the staging addresses: the 16-byte quad index within each 128-byte row is
+// XORed with the row index (mod 8).  Their lanes store the integers of a slot
+// 16 positions apart -- two banks for the whole warp unswizzled -- while the
+// copy-out still reads whole aligned quads.  Other ranges spread their stores
+// irregularly over the banks already and keep the plain layout (the swizzle
+// costs two ALU instructions per slot).
+__device__ __forceinline__ bool range_dense(unsigned long long ints, long long bytes) {
+    return bytes > 0 && 8ull * ints >= 7ull * static_cast<unsigned long long>(bytes);
+}
+template <bool kSwz>
+__device__ __forceinline__ uint32_t stg_addr(uint32_t b) { return kSwz ? b ^ ((b >> 3) & 0x70u) : b; }
+template <bool kSwz>
+__device__ __forceinline__ void sts_stage(uint32_t b, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(stg_addr<kSwz>(b)), "r"(v) : "memory");
+}
 
 // 7-bit digits of the four bytes of w, packed LSB first (28 bits).
 __device__ __forceinline__ uint32_t pack28(uint32_t w) {
@@ -615,7 +632,7 @@ __device__ __forceinline__ uint32_t lane_scan_offset(uint32_t total, uint32_t& c
 // m = 2^(7 * length) (the integer's bits are the top 7 * length bits of top);
 // next m = p ? 2^7 : m * 2^7.  The multiplies run on the FMA pipe, leaving the
 // (half-rate) ALU pipe the predicate, the selects and the funnel shift.
-template <bool kDelta>
+template <bool kDelta, bool kSwz>
 __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
                                                 uint32_t T16, uint32_t sp, uint32_t& carry) {
     const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
@@ -654,36 +671,48 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint3
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const uint32_t top = __funnelshift_r(lo[e >> 2], hi[e >> 2], 3 + 7 * (e & 3));
-            asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-                         "and.b32 t, %3, %5;\n\t"
-                         "setp.ne.b32 p, t, 0;\n\t"
-                         "mul.hi.u32 t, %4, %2;\n\t"
-                         "@p add.u32 %1, %1, t;\n\t"
-                         "@p st.shared.u32 [%0], %1;\n\t"
-                         "@p add.u32 %0, %0, 4;\n\t"
-                         "mul.lo.u32 t, %2, 128;\n\t"
-                         "selp.b32 %2, 128, t, p;\n\t"
-                         "}"
-                         : "+r"(sp), "+r"(acc), "+r"(m)
-                         : "r"(T16), "r"(top), "r"(1u << e)
-                         : "memory");
+#define MVB_SLOT_DELTA(STORE)                                                          \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
+                 "and.b32 t, %3, %5;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "mul.hi.u32 t, %4, %2;\n\t"                                             \
+                 "@p add.u32 %1, %1, t;\n\t" STORE                                       \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "mul.lo.u32 t, %2, 128;\n\t"                                            \
+                 "selp.b32 %2, 128, t, p;\n\t"                                           \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(acc), "+r"(m)                                             \
+                 : "r"(T16), "r"(top), "r"(1u << e)                                         \
+                 : "memory")
+            if (kSwz)
+                MVB_SLOT_DELTA("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
+                               "@p st.shared.u32 [t], %1;\n\t");
+            else
+                MVB_SLOT_DELTA("@p st.shared.u32 [%0], %1;\n\t");
+#undef MVB_SLOT_DELTA
         }
     } else {
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const uint32_t top = __funnelshift_r(lo[e >> 2], hi[e >> 2], 3 + 7 * (e & 3));
-            asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
-                         "and.b32 t, %2, %4;\n\t"
-                         "setp.ne.b32 p, t, 0;\n\t"
-                         "mul.hi.u32 t, %3, %1;\n\t"
-                         "@p st.shared.u32 [%0], t;\n\t"
-                         "@p add.u32 %0, %0, 4;\n\t"
-                         "mul.lo.u32 t, %1, 128;\n\t"
-                         "selp.b32 %1, 128, t, p;\n\t"
-                         "}"
-                         : "+r"(sp), "+r"(m)
-                         : "r"(T16), "r"(top), "r"(1u << e)
-                         : "memory");
+#define MVB_SLOT_PLAIN(STORE)                                                          \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"                           \
+                 "and.b32 t, %2, %4;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "mul.hi.u32 t, %3, %1;\n\t" STORE                                       \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "mul.lo.u32 t, %1, 128;\n\t"                                            \
+                 "selp.b32 %1, 128, t, p;\n\t"                                           \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(m)                                                        \
+                 : "r"(T16), "r"(top), "r"(1u << e)                                         \
+                 : "memory")
+            if (kSwz)
+                MVB_SLOT_PLAIN("shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
+                               "@p st.shared.u32 [a], t;\n\t");
+            else
+                MVB_SLOT_PLAIN("@p st.shared.u32 [%0], t;\n\t");
+#undef MVB_SLOT_PLAIN
         }
     }
 }
@@ -691,9 +720,9 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint3
 // General slots: integers of 1..5 bytes, terminators restricted to ends16
 // (bytes outside the range), malformed runs decode to garbage (their index
 // is reported by ll_slice_gen; nothing after it is meaningful).
-template <bool kDelta>
+template <bool kDelta, bool kSwz>
 __device__ __forceinline__ void lane_slots_gen(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
-                                               uint32_t T16, uint32_t ends16, uint32_t* sp, uint32_t& carry) {
+                                               uint32_t T16, uint32_t ends16, uint32_t sp, uint32_t& carry) {
     const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
     const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
     const uint32_t hi[4] = {c0 >> 4, c1 >> 4, c2 >> 4, c3 >> 4};
@@ -711,24 +740,28 @@ __device__ __forceinline__ void lane_slots_gen(uint32_t wp3, uint32_t w0, uint32
             if ((ends16 >> e) & 1u) acc += v;
             val[e] = acc;
         } else if ((ends16 >> e) & 1u) {
-            *sp++ = v;
+            sts_stage<kSwz>(sp, v);
+            sp += 4;
         }
     }
     if (kDelta) {
         const uint32_t ex = lane_scan_offset<kDelta>(acc, carry);
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-            if ((ends16 >> e) & 1u) *sp++ = val[e] + ex;
+            if ((ends16 >> e) & 1u) {
+                sts_stage<kSwz>(sp, val[e] + ex);
+                sp += 4;
+            }
     }
 }
 
 // The general path of one slice (after the count scan): malformed integers,
 // the end of integer limit-1, then the general slots.
-template <bool kDelta>
+template <bool kDelta, bool kSwz>
 __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
                                           uint32_t w3, uint32_t wp3, uint32_t T16, uint32_t inr16, uint32_t n_own,
                                           uint32_t n_w, uint32_t wexcl, unsigned long long rs,
-                                          unsigned long long limit, const RangeSink& K, uint32_t* sp,
+                                          unsigned long long limit, const RangeSink& K, uint32_t sp,
                                           uint32_t& carry) {
     const int lane = threadIdx.x & 31;
     const uint32_t ends16 = T16 & inr16;
@@ -771,14 +804,15 @@ __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, uint
         for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
         sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
     }
-    lane_slots_gen<kDelta>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
+    lane_slots_gen<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
 }
 
 // Copy stage[a, a + n) to out[run, run + n), indices below `limit` only;
 // stage[i] <-> out[run - a + i] with out + run - a 16-byte aligned.  Whole
 // quads in the loop; the partial first quad [a, 4) and last quad
 // [end & ~3, end) by lanes 0..3 and 4..7, one integer each.
-__device__ __forceinline__ void stage_out(const uint32_t* stage, uint32_t a, uint32_t n, unsigned long long run,
+template <bool kSwz>
+__device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t n, unsigned long long run,
                                           unsigned long long limit, uint32_t* out, int lane) {
     if (run >= limit) return;
     const unsigned long long g0 = run - a;
@@ -788,10 +822,20 @@ __device__ __forceinline__ void stage_out(const uint32_t* stage, uint32_t a, uin
     const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
     if (lane < 8) {
         const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
-        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) ob[i] = stage[i];
+        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(stg_addr<kSwz>(st_base + 4u * i)) : "memory");
+            ob[i] = v;
+        }
     }
-    for (uint32_t i = i0 + 4 * lane; i < i1; i += 128)
-        *reinterpret_cast<uint4*>(ob + i) = *reinterpret_cast<const uint4*>(stage + i);
+    for (uint32_t i = i0 + 4 * lane; i < i1; i += 128) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(stg_addr<kSwz>(st_base + 4u * i))
+                     : "memory");
+        *reinterpret_cast<uint4*>(ob + i) = v;
+    }
 }
 
 // cp.async prefetch of the next slice into a warp's 2 x 512-byte ring
@@ -806,7 +850,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // are indexed from qs; interior slices (inside [R.lo, R.hi)) arrive by
 // cp.async one slice ahead into ring half (i & 1), the others are read with
 // range masks.
-template <bool kDelta>
+template <bool kDelta, bool kSwz>
 __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs, long long qe,
                                                 unsigned long long base, uint32_t carry, unsigned long long limit,
                                                 uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
@@ -883,17 +927,17 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             const bool fast = !__any_sync(0xFFFFFFFFu, run4) && inter && n_w < left;
             if (n_w) last_i = i;
             if (fast)
-                lane_slots_fast<kDelta>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
+                lane_slots_fast<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
             else
-                ll_slice_gen<kDelta>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3, wp3,
-                                     T16, inr16, n_own, n_w, wexcl, run + n_g, limit, K, stage + a + n_g + wexcl,
-                                     carry);
+                ll_slice_gen<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3,
+                                           wp3, T16, inr16, n_own, n_w, wexcl, run + n_g, limit, K,
+                                           st_base + 4u * (a + n_g + wexcl), carry);
             n_g += n_w;
             left = left > n_w ? left - n_w : 0u;
         }
         if (n_g == 0) continue;
         __syncwarp();
-        stage_out(stage, a, n_g, run, limit, out, lane);
+        stage_out<kSwz>(st_base, a, n_g, run, limit, out, lane);
         run += n_g;
         __syncwarp();  // the staging buffer is rewritten by the next group
     }
@@ -966,9 +1010,18 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_de
             kDelta ? static_cast<uint32_t>(csum) - straddle + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
         RangeOut ro;
         const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
-        if (kLL)
-            decode_range_ll<kDelta>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
-                                    reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+        if (kLL) {
+            // integers in the run (segments s .. s_end - 1, at most 32 when kLL): its density
+            unsigned long long rc = (s + lane < s_end) ? S.scnt[s + lane] : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
+            if (range_dense(rc, (s_end - s) * S.seg_bytes))
+                decode_range_ll<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                                              reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+            else
+                decode_range_ll<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                                               reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+        }
         else
             decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
                                  lane, K, ro);
@@ -1093,8 +1146,12 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) 
             const RangeSink K = {nullptr, &s_err_idx[wid], &s_err_pos[wid], &s_count_end[wid]};
             const uint32_t carry = kDelta && L.prev ? L.prev[l] : 0u;
             if (kLL)
-                decode_range_ll<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
-                                        reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+                if (range_dense(cnt, R.hi - R.lo))
+                    decode_range_ll<kDelta, true>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
+                                                  reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+                else
+                    decode_range_ll<kDelta, false>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
+                                                   reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
             else
                 decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out, vbase, eph, lane, K, ro);
             __syncwarp();
