@@ -1,49 +1,40 @@
-"""Stall samples per CUDA source line with the dominant reasons."""
-import csv
-import io
-import subprocess
-import sys
-from collections import defaultdict
+"""Per CUDA source line of one kernel: warp-stall samples by reason (deduped by
+SASS address, attributed to the innermost source line).
+usage: ncu_stall_lines.py REP KERNEL_REGEX [N]"""
+import csv, io, subprocess, sys, collections
 
-rep = sys.argv[1]
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-hdr = None
-cur = None
-agg = defaultdict(lambda: defaultdict(int))
-func = None
-cf = None
-for r in rows:
+rep, kern = sys.argv[1], sys.argv[2]
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+raw = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kern, "--page", "source", "--csv", "--print-source",
+                      "cuda,sass"], capture_output=True, text=True).stdout
+reasons = ["stall_barrier", "stall_branch_resolving", "stall_dispatch", "stall_lg", "stall_long_sb", "stall_math",
+           "stall_mio", "stall_no_inst", "stall_not_selected", "stall_selected", "stall_short_sb", "stall_wait"]
+fname, line, hdr = "", "", None
+seen = {}
+for r in csv.reader(io.StringIO(raw)):
     if not r:
         continue
     if r[0] == "File Path":
-        cf = r[1].split("/")[-1]
-        continue
-    if r[0] == "Function Name":
-        if func and r[1] != func:
-            break
-        func = r[1]
+        fname = r[1].split("/")[-1]
         continue
     if r[0] == "Line No":
-        hdr = r
+        hdr = {k: i for i, k in enumerate(r)}
         continue
-    if not hdr:
+    if hdr is None or r[0] == "Function Name":
         continue
     if r[0]:
-        cur = (cf, int(r[0]), r[1][:60])
-    d = dict(zip(hdr[2:], r[2:]))
-    if not d.get("Address"):
+        line = f"{fname}:{r[0]}"
         continue
-    for k, v in d.items():
-        if k.startswith("stall_") and "Not Issued" not in k:
-            try:
-                agg[cur][k] += int(v or 0)
-            except ValueError:
-                pass
-tot = sum(sum(v.values()) for v in agg.values()) or 1
-for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1].values()))[:n]:
-    s = sum(v.values())
-    top = sorted(v.items(), key=lambda x: -x[1])[:3]
-    print(f"{100 * s / tot:5.1f}% {k[0]}:{k[1]} {k[2][:55]:55s} " + " ".join(f"{a[6:]}={100 * b / s:.0f}%" for a, b in top))
+    try:
+        seen[r[2]] = (line, {k: int(r[hdr[k]] or 0) for k in reasons})
+    except (ValueError, IndexError, KeyError):
+        pass
+agg = collections.defaultdict(collections.Counter)
+for line, d in seen.values():
+    agg[line].update(d)
+tot = sum(sum(c.values()) for c in agg.values())
+print("total samples", tot)
+for line, c in sorted(agg.items(), key=lambda kv: -sum(kv[1].values()))[:n]:
+    s = sum(c.values())
+    top = ", ".join(f"{k[6:]} {v}" for k, v in c.most_common(3) if v)
+    print(f"{100.0 * s / tot:5.1f}%  {line:28s} {top}")
