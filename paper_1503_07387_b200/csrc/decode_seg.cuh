@@ -218,6 +218,7 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         nx[c] = (0 >= i_lo && 0 < i_hi) ? ldg_stream16(pin + 16 * c) : seg_load16(S, q_begin + L * lane + 16 * c);
     unsigned cnt = 0;
     uint32_t sum = 0;
+    unsigned long long gc = 0, gs = 0;  // totals of the run's segments in the current group
     long long s = s_begin;
     int it_s = 0;  // iteration within segment s
     for (int it = 0; it < n_it; ++it) {
@@ -268,18 +269,21 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         }
         if (seg_last) {
             const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
-            uint32_t s_tot = sum;
-            if (kDelta) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s_tot += __shfl_xor_sync(0xFFFFFFFFu, s_tot, o);
-            }
+            const uint32_t s_tot = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sum) : 0u;
             if (lane == 0) {
                 S.scnt[s] = c_tot;
-                atomicAdd(S.gcnt + (s >> 5), static_cast<unsigned long long>(c_tot));
-                if (kDelta) {
-                    S.ssum[s] = s_tot;
-                    atomicAdd(S.gsum + (s >> 5), static_cast<unsigned long long>(s_tot));
+                if (kDelta) S.ssum[s] = s_tot;
+            }
+            // group accumulators: one atomic per group the run touches
+            gc += c_tot;
+            gs += s_tot;
+            if (((s + 1) & 31) == 0 || s + 1 == s_end) {
+                if (lane == 0) {
+                    atomicAdd(S.gcnt + (s >> 5), gc);
+                    if (kDelta) atomicAdd(S.gsum + (s >> 5), gs);
                 }
+                gc = 0;
+                gs = 0;
             }
             cnt = 0;
             sum = 0;
@@ -578,10 +582,15 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 #ifndef MVB_LL_BLOCKS
 #define MVB_LL_BLOCKS 6
 #endif
-constexpr int kLLBlocks = MVB_LL_BLOCKS;           // resident CTAs per SM the register budget targets
-constexpr int kLaneGroup = 2;                      // slices per staging copy-out
+#ifndef MVB_LL_BLOCKS_DELTA
+#define MVB_LL_BLOCKS_DELTA 6
+#endif
+constexpr int kLLBlocks = MVB_LL_BLOCKS;           // resident CTAs per SM the register budget targets (plain)
+constexpr int kLLBlocksD = MVB_LL_BLOCKS_DELTA;    // (delta: the running sum and its prefix)
+constexpr int kLLSlice = 1024;                     // bytes per slice: 32 lanes x 32 bytes
+constexpr int kLaneGroup = 2;                      // (V/EP-sized staging: 2 x 512 integers)
 constexpr int kLaneStage = kLaneGroup * 512 + 32;  // staging words per warp (+ alignment), whole 128-byte rows
-constexpr int kLaneWarpBytes = 4 * kLaneStage + 1024;  // staging + 2 x 512-byte input ring
+constexpr int kLaneWarpBytes = 4 * kLaneStage + 2 * kLLSlice;  // staging + 2-slice input ring
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
 static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
 
@@ -627,13 +636,15 @@ __device__ __forceinline__ uint32_t lane_scan_offset(uint32_t total, uint32_t& c
     return ex;
 }
 
+// ---- 16-byte lanes (delta decodes): 512-byte slices, two per staging group ----
+
 // Fast slots (see above): sp = shared-memory address of the lane's first
 // output.  Per slot e: p = byte e terminates; v = umulhi(top, m) with
 // m = 2^(7 * length) (the integer's bits are the top 7 * length bits of top);
 // next m = p ? 2^7 : m * 2^7.  The multiplies run on the FMA pipe, leaving the
 // (half-rate) ALU pipe the predicate, the selects and the funnel shift.
 template <bool kDelta, bool kSwz>
-__device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+__device__ __forceinline__ void lane_slots_fast16(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
                                                 uint32_t T16, uint32_t sp, uint32_t& carry) {
     const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
     const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
@@ -721,7 +732,7 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, uint32_t w0, uint3
 // (bytes outside the range), malformed runs decode to garbage (their index
 // is reported by ll_slice_gen; nothing after it is meaningful).
 template <bool kDelta, bool kSwz>
-__device__ __forceinline__ void lane_slots_gen(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+__device__ __forceinline__ void lane_slots_gen16(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
                                                uint32_t T16, uint32_t ends16, uint32_t sp, uint32_t& carry) {
     const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
     const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
@@ -758,7 +769,7 @@ __device__ __forceinline__ void lane_slots_gen(uint32_t wp3, uint32_t w0, uint32
 // The general path of one slice (after the count scan): malformed integers,
 // the end of integer limit-1, then the general slots.
 template <bool kDelta, bool kSwz>
-__device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
+__device__ __noinline__ void ll_slice_gen16(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
                                           uint32_t w3, uint32_t wp3, uint32_t T16, uint32_t inr16, uint32_t n_own,
                                           uint32_t n_w, uint32_t wexcl, unsigned long long rs,
                                           unsigned long long limit, const RangeSink& K, uint32_t sp,
@@ -804,7 +815,216 @@ __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, uint
         for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
         sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
     }
-    lane_slots_gen<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
+    lane_slots_gen16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
+}
+
+// ---- 32-byte lanes (plain decodes): 1 KiB slices ----
+
+// Fast slots (see above) of a lane's 32 bytes w[0..7]; sp = shared-memory
+// address of the lane's first output.  Per slot e: p = byte e terminates;
+// v = umulhi(top, m) with m = 2^(7 * length) (the integer's bits are the top
+// 7 * length bits of top); next m = p ? 2^7 : m * 2^7.  The multiplies run on
+// the FMA pipe, leaving the (half-rate) ALU pipe the predicate, the select
+// and the funnel shift.  Delta: the lane's exclusive prefix comes first (SWAR
+// digit-weight sum, warp scan), then each slot stores the running sum.
+template <bool kDelta, bool kSwz>
+__device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w)[8], uint32_t T32, uint32_t sp,
+                                                uint32_t& carry) {
+    const uint32_t tp = hibits4(~wp3);
+    const uint32_t cm = pack28(wp3);
+    // length of the integer ending at byte 0 = 4 - (last terminator among bytes -4..-1)
+    uint32_t m = 1u << (28 - 7 * (31 - __clz(static_cast<int>(tp))));
+    uint32_t acc = 0;
+    if (kDelta) {
+        // digit-weight sum of the 32 bytes, minus the tail (bytes after the last
+        // terminator: c7 >> 7 * (t + 1)), plus the head (the same for the 4 bytes
+        // before: the previous lane's tail)
+        const uint32_t t7 = 31 - __clz(static_cast<int>(T32 >> 28));
+        uint32_t S = 0, hic = 0, pv = wp3;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t ck = w[k] & 0x80808080u, cp = pv & 0x80808080u;
+            const uint32_t c1b = __funnelshift_l(cp, ck, 1);
+            hic |= c1b & __funnelshift_l(cp, ck, 9);
+            S = __dp4a(w[k] & 0x7F7F7F7Fu, c1b * 127u + 0x01010101u, S);
+            pv = w[k];
+        }
+        if (__any_sync(0xFFFFFFFFu, hic)) {  // bytes after 2 or 3 continuation bytes: 2^14 / 2^21, not 128
+            pv = wp3;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t ck = w[k] & 0x80808080u, cp = pv & 0x80808080u;
+                const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+                const uint32_t c3 = __funnelshift_l(cp, ck, 24);
+                const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
+                S += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3), 0u) << 14;
+                S -= __dp4a(b, cc >> 7, 0u) << 7;
+                pv = w[k];
+            }
+        }
+        const uint32_t own =
+            S - shr_clamp(pack28(w[7]), 7 * (t7 + 1)) + shr_clamp(cm, 7 * (32 - __clz(static_cast<int>(tp))));
+        acc = lane_scan_offset<kDelta>(own, carry);
+    }
+    uint32_t cprev = cm;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t ck = pack28(w[k]);
+        const uint32_t lo = cprev + (ck << 28), hi = ck >> 4;
+        cprev = ck;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int e = 4 * k + t;
+            const uint32_t top = __funnelshift_r(lo, hi, 3 + 7 * t);
+            if (kDelta) {
+#define MVB_SLOT_DELTA(STORE)                                                          \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
+                 "and.b32 t, %3, %5;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "mul.hi.u32 t, %4, %2;\n\t"                                             \
+                 "@p add.u32 %1, %1, t;\n\t" STORE                                       \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "mul.lo.u32 t, %2, 128;\n\t"                                            \
+                 "selp.b32 %2, 128, t, p;\n\t"                                           \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(acc), "+r"(m)                                             \
+                 : "r"(T32), "r"(top), "r"(1u << e)                                         \
+                 : "memory")
+                if (kSwz)
+                    MVB_SLOT_DELTA("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
+                                   "@p st.shared.u32 [t], %1;\n\t");
+                else
+                    MVB_SLOT_DELTA("@p st.shared.u32 [%0], %1;\n\t");
+#undef MVB_SLOT_DELTA
+            } else {
+#define MVB_SLOT_PLAIN(STORE)                                                          \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"                           \
+                 "and.b32 t, %2, %4;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "mul.hi.u32 t, %3, %1;\n\t" STORE                                       \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "mul.lo.u32 t, %1, 128;\n\t"                                            \
+                 "selp.b32 %1, 128, t, p;\n\t"                                           \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(m)                                                        \
+                 : "r"(T32), "r"(top), "r"(1u << e)                                         \
+                 : "memory")
+                if (kSwz)
+                    MVB_SLOT_PLAIN("shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
+                                   "@p st.shared.u32 [a], t;\n\t");
+                else
+                    MVB_SLOT_PLAIN("@p st.shared.u32 [%0], t;\n\t");
+#undef MVB_SLOT_PLAIN
+            }
+        }
+    }
+}
+
+// General slots of one 16-byte half (integers of 1..5 bytes, terminators
+// restricted to ends16 = bytes inside the range; malformed runs decode to
+// garbage -- their index is reported by ll_slice_gen, nothing after it is
+// meaningful).  kMode 0: return the sum of the half's integers; 1: store
+// them; 2: store the running sum starting from acc.
+template <int kMode, bool kSwz>
+__device__ __forceinline__ uint32_t gen_half(uint32_t wp3, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                             uint32_t T16, uint32_t ends16, uint32_t sp, uint32_t acc) {
+    const uint32_t cm = pack28(wp3), c0 = pack28(w0), c1 = pack28(w1), c2 = pack28(w2), c3 = pack28(w3);
+    const uint32_t lo[4] = {cm + (c0 << 28), c0 + (c1 << 28), c1 + (c2 << 28), c2 + (c3 << 28)};
+    const uint32_t hi[4] = {c0 >> 4, c1 >> 4, c2 >> 4, c3 >> 4};
+    int sh = 7 * (31 - __clz(static_cast<int>(hibits4(~wp3)))) + 4;  // -3 if no terminator in the 4 bytes before
+    uint32_t sum = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        if (e) sh = ((T16 >> (e - 1)) & 1u) ? 25 : sh - 7;
+        const int k = e >> 2, t = e & 3;
+        const uint32_t top = __funnelshift_r(lo[k], hi[k], 3 + 7 * t);  // packed bits ending with byte e
+        uint32_t v = shr_clamp(top, sh);
+        if (sh < 0) v = __funnelshift_r(lo[k], hi[k], 7 * t);  // five bytes: the low 32 bits
+        if ((ends16 >> e) & 1u) {
+            if (kMode == 0) {
+                sum += v;
+            } else {
+                if (kMode == 2) acc += v;
+                sts_stage<kSwz>(sp, kMode == 2 ? acc : v);
+                sp += 4;
+            }
+        }
+    }
+    return sum;
+}
+
+// Strict checks of one 16-byte half: the first malformed integer (a fifth byte
+// >= 0x10, i.e. 4 continuation bytes after an integer end, then anything but
+// 0x00..0x0F) and the end of integer limit-1.
+__device__ __forceinline__ void gen_check_half(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1,
+                                               uint32_t w2, uint32_t w3, uint32_t wp2, uint32_t wp3, uint32_t T16,
+                                               uint32_t inr16, uint32_t n_w, uint32_t wexcl,
+                                               unsigned long long rs, unsigned long long limit,
+                                               const RangeSink& K) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ends16 = T16 & inr16;
+    const uint32_t n_own = __popc(ends16);
+    const uint32_t Tx = hibits4(~wp2) | (hibits4(~wp3) << 4) | (T16 << 8);  // positions -8..15
+    const uint32_t Cx = ~Tx & 0x00FFFFFFu;
+    const uint32_t run4 = Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3);
+    uint32_t bad16 = 0;
+    if (run4) {
+        const uint32_t five = (Tx >> 3) & (run4 >> 4) & inr16;
+        if (five) {
+            const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
+            const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
+            const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
+            const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
+            bad16 = five & hibits16(g0, g1, g2, g3);
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the half's first malformed integer
+        const int j = bad16 ? __ffs(bad16) - 1 : 0;
+        unsigned long long idx = bad16 ? rs + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
+        long long pos = q0 + j - 4 - R.lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+            const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
+            if (oi < idx) {
+                idx = oi;
+                pos = op;
+            }
+        }
+        if (lane == 0) sink_error(K, idx, pos, limit);
+    }
+    if (n_w && limit - rs <= n_w && limit - 1 - rs >= wexcl && limit - 1 - rs < wexcl + n_own) {
+        uint32_t m = ends16;
+        for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
+        sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
+    }
+}
+
+// The general path of one slice (lane = 32 bytes w[0..7], as two 16-byte
+// halves): strict checks, then the general slots.  Delta: both halves' sums
+// first (the output order is lane-major), one warp scan, then the stores.
+template <bool kDelta, bool kSwz>
+__device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
+                                          uint32_t wp2, uint32_t wp3, uint32_t T32, uint32_t inr32, uint32_t n_w,
+                                          uint32_t wexcl, unsigned long long rs, unsigned long long limit,
+                                          const RangeSink& K, uint32_t sp, uint32_t& carry) {
+    const uint32_t e0 = T32 & inr32 & 0xFFFFu, e1 = (T32 & inr32) >> 16;
+    gen_check_half(R, q0, x0.x, x0.y, x0.z, x0.w, wp2, wp3, T32 & 0xFFFFu, inr32 & 0xFFFFu, n_w, wexcl, rs, limit,
+                   K);
+    gen_check_half(R, q0 + 16, x1.x, x1.y, x1.z, x1.w, x0.z, x0.w, T32 >> 16, inr32 >> 16, n_w,
+                   wexcl + __popc(e0), rs, limit, K);
+    if (n_w == 0) return;
+    const uint32_t sp1 = sp + 4u * __popc(e0);
+    if (kDelta) {
+        const uint32_t s0 = gen_half<0, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, 0u, 0u);
+        const uint32_t s1 = gen_half<0, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, 0u, 0u);
+        const uint32_t ex = lane_scan_offset<kDelta>(s0 + s1, carry);
+        gen_half<2, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, sp, ex);
+        gen_half<2, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, ex + s0);
+    } else {
+        gen_half<1, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, sp, 0u);
+        gen_half<1, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, 0u);
+    }
 }
 
 // Copy stage[a, a + n) to out[run, run + n), indices below `limit` only;
@@ -838,20 +1058,149 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
     }
 }
 
-// cp.async prefetch of the next slice into a warp's 2 x 512-byte ring
+// cp.async prefetch of the next slice into a warp's 2 x kLLSlice-byte ring
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 x;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(a) : "memory");
+    return x;
+}
 
-// ring: shared-memory address of the warp's 2 x 512-byte input ring.  Slices
+// ring: shared-memory address of the warp's 2 x kLLSlice-byte input ring.
+// Slices (kLLSlice bytes: 32 per lane) are indexed from qs; interior slices
+// (inside [R.lo, R.hi)) arrive by cp.async one slice ahead into ring half
+// (i & 1), the others are read with range masks.
+template <bool kDelta, bool kSwz>
+__device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs, long long qe,
+                                                unsigned long long base, uint32_t carry, unsigned long long limit,
+                                                uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
+                                                const RangeSink& K, RangeOut& ro) {
+    const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
+    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const int ns = static_cast<int>((qe - qs + kLLSlice - 1) / kLLSlice);
+    int i_lo, i_hi;  // interior slices: i_lo <= i < i_hi
+    {
+        const long long d = R.lo - qs, e = R.hi - qs;
+        const long long lo = d <= 0 ? 0 : (d + kLLSlice - 1) / kLLSlice;
+        const long long hi = e <= 0 ? 0 : e / kLLSlice;
+        i_lo = static_cast<int>(lo < ns ? lo : ns);
+        i_hi = static_cast<int>(hi < ns ? hi : ns);
+    }
+    const uint8_t* const pin = R.ab + qs + 32 * lane;  // this lane's bytes of slice 0
+    const uint32_t rbase = ring + 32u * lane;
+    // integers that may still be stored before `limit` (clamped): a slice with fewer takes the fast path
+    uint32_t left;
+    {
+        const unsigned long long r = limit > base ? limit - base : 0ull;
+        left = r > 0x7FFFFFFFull ? 0x7FFFFFFFu : static_cast<uint32_t>(r);
+    }
+    unsigned long long run = base;  // output index of the slice's first integer
+    int last_i = -1;                // the last slice holding an integer (warp-uniform)
+    uint32_t pw2 = 0, pw3 = 0;      // lane 0: the 8 bytes before the slice
+    if (lane == 0) {
+        if (r_inside(R, qs - 8, 8)) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(R.ab + qs - 8));
+            pw2 = v.x;
+            pw3 = v.y;
+        } else {
+            pw2 = r_word(R, qs - 8);
+            pw3 = r_word(R, qs - 4);
+        }
+    }
+    if (i_lo == 0 && i_hi > 0) {
+        cp_async16(rbase, pin);
+        cp_async16(rbase + 16, pin + 16);
+        cp_async_commit();
+    }
+#pragma unroll 1
+    for (int i = 0; i < ns; ++i) {
+        const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
+        const bool inter = i >= i_lo && i < i_hi;                      // warp-uniform
+        const bool pfn = i + 1 >= i_lo && i + 1 < i_hi;
+        if (pfn) {
+            const uint32_t d = rbase + kLLSlice * ((i + 1) & 1);
+            cp_async16(d, pin + kLLSlice * (i + 1));
+            cp_async16(d + 16, pin + kLLSlice * (i + 1) + 16);
+            cp_async_commit();
+        }
+        const long long q0 = qs + static_cast<long long>(kLLSlice) * i + 32 * lane;
+        uint4 x0, x1;
+        if (inter) {
+            if (pfn) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            x0 = lds128(rbase + kLLSlice * (i & 1));
+            x1 = lds128(rbase + kLLSlice * (i & 1) + 16);
+        } else {
+            x0 = r_load16(R, q0);
+            x1 = r_load16(R, q0 + 16);
+        }
+        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1), wp2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
+        const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31), l2 = __shfl_sync(0xFFFFFFFFu, w[6], 31);
+        if (lane == 0) {
+            wp3 = pw3;
+            wp2 = pw2;
+        }
+        pw3 = l3;
+        pw2 = l2;
+        const uint32_t T32 = hibits16(~w[0], ~w[1], ~w[2], ~w[3]) | (hibits16(~w[4], ~w[5], ~w[6], ~w[7]) << 16);
+        const uint32_t inr32 = inter ? 0xFFFFFFFFu : (r_inr16(R, q0) | (r_inr16(R, q0 + 16) << 16));
+        const uint32_t n_own = __popc(T32 & inr32);
+        uint32_t incl = n_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t wexcl = incl - n_own;
+        // four continuation bytes in a row anywhere in positions -4..31
+        const unsigned long long C = ((static_cast<unsigned long long>(~T32) << 4) | (~hibits4(~wp3) & 0xFu));
+        const unsigned long long run4 = C & (C >> 1) & (C >> 2) & (C >> 3) & 0x1FFFFFFFFull;
+        const bool fast = !__any_sync(0xFFFFFFFFu, run4 != 0) && inter && n_w < left;
+        if (n_w) last_i = i;
+        if (fast)
+            lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+        else
+            ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
+                                       st_base + 4u * (a + wexcl), carry);
+        left = left > n_w ? left - n_w : 0u;
+        if (n_w == 0) continue;
+        __syncwarp();
+        stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
+        run += n_w;
+        __syncwarp();  // the staging buffer is rewritten by the next slice
+    }
+    // the end of the range's last integer: in slice last_i
+    long long last_end = -1;
+    if (last_i >= 0) {
+        const long long q0 = qs + static_cast<long long>(kLLSlice) * last_i + 32 * lane;
+        const uint4 x0 = r_load16(R, q0), x1 = r_load16(R, q0 + 16);
+        const uint32_t e0 = hibits16(~x0.x, ~x0.y, ~x0.z, ~x0.w) & r_inr16(R, q0);
+        const uint32_t e1 = hibits16(~x1.x, ~x1.y, ~x1.z, ~x1.w) & r_inr16(R, q0 + 16);
+        if (e1) last_end = q0 + 16 + (31 - __clz(e1)) + 1 - R.lo;
+        else if (e0) last_end = q0 + (31 - __clz(e0)) + 1 - R.lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long le = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
+            last_end = le > last_end ? le : last_end;
+        }
+    }
+    ro.last_end = last_end;
+    ro.n = run - base;
+}
+
+// 16-byte-lane range decode (delta); ring: the warp's input ring (2 x 512 bytes used).  Slices
 // are indexed from qs; interior slices (inside [R.lo, R.hi)) arrive by
 // cp.async one slice ahead into ring half (i & 1), the others are read with
 // range masks.
 template <bool kDelta, bool kSwz>
-__device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs, long long qe,
+__device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long qs, long long qe,
                                                 unsigned long long base, uint32_t carry, unsigned long long limit,
                                                 uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
                                                 const RangeSink& K, RangeOut& ro) {
@@ -927,9 +1276,9 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             const bool fast = !__any_sync(0xFFFFFFFFu, run4) && inter && n_w < left;
             if (n_w) last_i = i;
             if (fast)
-                lane_slots_fast<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
+                lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
             else
-                ll_slice_gen<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3,
+                ll_slice_gen16<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3,
                                            wp3, T16, inr16, n_own, n_w, wexcl, run + n_g, limit, K,
                                            st_base + 4u * (a + n_g + wexcl), carry);
             n_g += n_w;
@@ -958,9 +1307,21 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     ro.n = run - base;
 }
 
+// The lane-local range decode: 16-byte lanes for delta decodes (their SWAR
+// prefix and running sums keep within the 80-register budget), 32-byte lanes
+// for plain decodes (half the per-slice fixed work per byte).
+template <bool kDelta, bool kSwz>
+__device__ __forceinline__ void decode_range_llw(const ByteRange& R, long long qs, long long qe,
+                                                 unsigned long long base, uint32_t carry, unsigned long long limit,
+                                                 uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
+                                                 const RangeSink& K, RangeOut& ro) {
+    if (kDelta) decode_range_ll16<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
+    else decode_range_ll<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
+}
+
 // kLL: 0 decode_range (V / EP windows), 1 decode_range_ll (lane-local)
 template <bool kDelta, int kLL>
-__global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_decode(SegParams S) {
+__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 8) vbyte_seg_decode(SegParams S) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
     const int lane = threadIdx.x & 31;
@@ -1016,10 +1377,10 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? kLLBlocks : 8) vbyte_seg_de
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
             if (range_dense(rc, (s_end - s) * S.seg_bytes))
-                decode_range_ll<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                decode_range_llw<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
                                               reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
             else
-                decode_range_ll<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                decode_range_llw<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
                                                reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
         }
         else
@@ -1108,7 +1469,7 @@ struct ListParams {
 };
 
 template <bool kDelta, int kLL>
-__global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) {
+__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 1) vbyte_lists_decode(ListParams L) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
     __shared__ unsigned long long s_err_idx[kSegWarps];
@@ -1147,10 +1508,10 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_lists_decode(ListParams L) 
             const uint32_t carry = kDelta && L.prev ? L.prev[l] : 0u;
             if (kLL)
                 if (range_dense(cnt, R.hi - R.lo))
-                    decode_range_ll<kDelta, true>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
+                    decode_range_llw<kDelta, true>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
                                                   reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
                 else
-                    decode_range_ll<kDelta, false>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
+                    decode_range_llw<kDelta, false>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
                                                    reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
             else
                 decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out, vbase, eph, lane, K, ro);

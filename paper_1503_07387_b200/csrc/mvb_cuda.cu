@@ -657,6 +657,6 @@ int mvbx_kernels_per_decode(int mode) {
     return (mode == MVB_STRICT && (g_kernel_choice == 0 || g_kernel_choice == 5)) ? 2 : 1;
 }
 
-const char* mvb_version(void) { return "mvb_cuda 0.1 (sm_100a, single-pass lookback VByte decoder)"; }
+const char* mvb_version(void) { return "mvb_cuda 0.2 (sm_100a, segmented lane-local VByte decoder)"; }
 
 }  // extern "C"
