@@ -91,6 +91,19 @@ __device__ __forceinline__ uint32_t seg_inr16(const SegParams& S, long long q0) 
     return (hi <= lo) ? 0u : ((0xFFFFu >> (16 - (hi - lo))) << lo) & 0xFFFFu;
 }
 
+// cp.async prefetch of 16 bytes into shared memory (per-thread groups)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 x;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(a) : "memory");
+    return x;
+}
+
 // ------------------------------------------------------------------ kernel A
 
 // Digit-weight sum of one word w (bytes b0..b3) given the 8 preceding bytes
@@ -131,6 +144,8 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
 constexpr int kSegAChunks = 2;                     // kernel A: 16-byte chunks per lane per iteration
 constexpr int kSegASlice = 512 * kSegAChunks;      // bytes per warp iteration
 constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + the lane's bytes
+constexpr int kAStages = 4;                        // kernel A: cp.async ring depth (iterations in flight)
+constexpr int kASmem = kSegWarps * kAStages * kSegASlice;
 
 // One warp walks a contiguous run of segments in kSegASlice-byte iterations
 // (lane l: 16*kSegAChunks contiguous bytes), prefetching the next iteration across segment
@@ -139,7 +154,8 @@ constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + t
 // (head, at most 4: lane 0's halo word) and leaves out the bytes after its
 // last terminator (tail, at most 4 in canonical data: lane 31's last words).
 template <bool kDelta>
-__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane);
+__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane,
+                                               uint32_t ring);
 
 template <bool kDelta>
 __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
@@ -147,7 +163,10 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const long long s_begin = gw * S.n_seg / nw, s_end = (gw + 1) * S.n_seg / nw;  // balanced runs
-    if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane);
+    extern __shared__ __align__(128) uint8_t smem_a[];
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem_a)) +
+                          static_cast<uint32_t>((threadIdx.x >> 5) * kAStages * kSegASlice);
+    if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane, ring);
 }
 
 // Digit-weight sums of a lane's words: weight 1 after a terminator, 128
@@ -186,7 +205,8 @@ __device__ __forceinline__ uint32_t words_digit_sum_hi(const uint32_t (&w)[kW]) 
 }
 
 template <bool kDelta>
-__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane) {
+__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane,
+                                               uint32_t ring) {
     const int its_per_seg = static_cast<int>(S.seg_bytes / kSegASlice);
     const long long q_begin = s_begin * S.seg_bytes, q_end = s_end * S.seg_bytes;
     const int n_it = static_cast<int>((q_end - q_begin) / kSegASlice);
@@ -212,32 +232,48 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
             pw3 = seg_word(S, q_begin - 4);
         }
     }
-    uint4 nx[kSegAChunks];
+    // interior iterations stream through a kAStages-deep cp.async ring (one
+    // commit group per iteration, possibly empty); the others load directly
+    const uint32_t rb = ring + L * lane;
 #pragma unroll
-    for (int c = 0; c < kSegAChunks; ++c)
-        nx[c] = (0 >= i_lo && 0 < i_hi) ? ldg_stream16(pin + 16 * c) : seg_load16(S, q_begin + L * lane + 16 * c);
+    for (int j = 0; j < kAStages - 1; ++j) {
+        if (j < n_it && j >= i_lo && j < i_hi) {
+#pragma unroll
+            for (int c = 0; c < kSegAChunks; ++c) cp_async16(rb + kSegASlice * j + 16 * c, pin + kSegASlice * j + 16 * c);
+        }
+        cp_async_commit();
+    }
     unsigned cnt = 0;
     uint32_t sum = 0;
     unsigned long long gc = 0, gs = 0;  // totals of the run's segments in the current group
     long long s = s_begin;
     int it_s = 0;  // iteration within segment s
     for (int it = 0; it < n_it; ++it) {
+        {
+            const int jn = it + kAStages - 1;
+            if (jn < n_it && jn >= i_lo && jn < i_hi) {
+                const uint32_t d = rb + kSegASlice * (jn & (kAStages - 1));
+#pragma unroll
+                for (int c = 0; c < kSegAChunks; ++c)
+                    cp_async16(d + 16 * c, pin + static_cast<long long>(kSegASlice) * jn + 16 * c);
+            }
+            cp_async_commit();
+        }
+        const bool inter = it >= i_lo && it < i_hi;
         uint32_t w[kSegAW];  // w[0], w[1]: the 8 bytes before this lane's bytes; then the lane's words
 #pragma unroll
         for (int c = 0; c < kSegAChunks; ++c) {
-            w[2 + 4 * c] = nx[c].x;
-            w[3 + 4 * c] = nx[c].y;
-            w[4 + 4 * c] = nx[c].z;
-            w[5 + 4 * c] = nx[c].w;
-        }
-        const bool inter = it >= i_lo && it < i_hi;
-        if (it + 1 < n_it) {
-            const bool inter_n = it + 1 >= i_lo && it + 1 < i_hi;
-#pragma unroll
-            for (int c = 0; c < kSegAChunks; ++c)
-                nx[c] = inter_n ? ldg_stream16(pin + static_cast<long long>(kSegASlice) * (it + 1) + 16 * c)
-                                : seg_load16(S, q_begin + static_cast<long long>(kSegASlice) * (it + 1) + L * lane +
-                                                    16 * c);
+            uint4 x;
+            if (inter) {
+                if (c == 0) cp_async_wait<kAStages - 1>();
+                x = lds128(rb + kSegASlice * (it & (kAStages - 1)) + 16 * c);
+            } else {
+                x = seg_load16(S, q_begin + static_cast<long long>(kSegASlice) * it + L * lane + 16 * c);
+            }
+            w[2 + 4 * c] = x.x;
+            w[3 + 4 * c] = x.y;
+            w[4 + 4 * c] = x.z;
+            w[5 + 4 * c] = x.w;
         }
         w[0] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 2], 1);
         w[1] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 1], 1);
@@ -579,6 +615,9 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 // integers, the end of integer limit-1).  Delta: in-lane running sums stay in
 // registers, the warp scan of the lane totals adds the offsets before the
 // stores.
+#ifndef MVB_DELTA32
+#define MVB_DELTA32 0  // 1: delta decodes on 32-byte lanes too (fewer instructions, longer dependency chains: slower on c2)
+#endif
 #ifndef MVB_LL_BLOCKS
 #define MVB_LL_BLOCKS 6
 #endif
@@ -875,20 +914,21 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int e = 4 * k + t;
-            const uint32_t top = __funnelshift_r(lo, hi, 3 + 7 * t);
+            const uint32_t fs = 3 + 7 * t;
             if (kDelta) {
 #define MVB_SLOT_DELTA(STORE)                                                          \
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
                  "and.b32 t, %3, %5;\n\t"                                                \
                  "setp.ne.b32 p, t, 0;\n\t"                                              \
-                 "mul.hi.u32 t, %4, %2;\n\t"                                             \
+                 "shf.r.wrap.b32 t, %6, %7, %4;\n\t"                                     \
+                 "mul.hi.u32 t, t, %2;\n\t"                                              \
                  "@p add.u32 %1, %1, t;\n\t" STORE                                       \
                  "@p add.u32 %0, %0, 4;\n\t"                                             \
                  "mul.lo.u32 t, %2, 128;\n\t"                                            \
                  "selp.b32 %2, 128, t, p;\n\t"                                           \
                  "}"                                                                        \
                  : "+r"(sp), "+r"(acc), "+r"(m)                                             \
-                 : "r"(T32), "r"(top), "r"(1u << e)                                         \
+                 : "r"(T32), "r"(fs), "r"(1u << e), "r"(lo), "r"(hi)                        \
                  : "memory")
                 if (kSwz)
                     MVB_SLOT_DELTA("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
@@ -901,13 +941,14 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"                           \
                  "and.b32 t, %2, %4;\n\t"                                                \
                  "setp.ne.b32 p, t, 0;\n\t"                                              \
-                 "mul.hi.u32 t, %3, %1;\n\t" STORE                                       \
+                 "shf.r.wrap.b32 t, %5, %6, %3;\n\t"                                     \
+                 "mul.hi.u32 t, t, %1;\n\t" STORE                                        \
                  "@p add.u32 %0, %0, 4;\n\t"                                             \
                  "mul.lo.u32 t, %1, 128;\n\t"                                            \
                  "selp.b32 %1, 128, t, p;\n\t"                                           \
                  "}"                                                                        \
                  : "+r"(sp), "+r"(m)                                                        \
-                 : "r"(T32), "r"(top), "r"(1u << e)                                         \
+                 : "r"(T32), "r"(fs), "r"(1u << e), "r"(lo), "r"(hi)                        \
                  : "memory")
                 if (kSwz)
                     MVB_SLOT_PLAIN("shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
@@ -1058,18 +1099,6 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
     }
 }
 
-// cp.async prefetch of the next slice into a warp's 2 x kLLSlice-byte ring
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-    uint4 x;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(a) : "memory");
-    return x;
-}
 
 // ring: shared-memory address of the warp's 2 x kLLSlice-byte input ring.
 // Slices (kLLSlice bytes: 32 per lane) are indexed from qs; interior slices
@@ -1315,7 +1344,7 @@ __device__ __forceinline__ void decode_range_llw(const ByteRange& R, long long q
                                                  unsigned long long base, uint32_t carry, unsigned long long limit,
                                                  uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
                                                  const RangeSink& K, RangeOut& ro) {
-    if (kDelta) decode_range_ll16<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
+    if (kDelta && !MVB_DELTA32) decode_range_ll16<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
     else decode_range_ll<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
 }
 

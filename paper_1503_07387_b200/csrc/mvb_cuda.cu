@@ -174,15 +174,18 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     static int per_sm_a = -1;
     if (per_sm_a < 0) {
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads, 0) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(mvbk::vbyte_seg_totals<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kASmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads,
+                                                          mvbk::kASmem) != cudaSuccess)
             return MVB_ERR_CUDA;
         per_sm_a = n > 0 ? n : 1;
     }
     const long long ga = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;  // at least one segment per warp
     const long long cap_a = static_cast<long long>(per_sm_a) * sms;
     const unsigned grid_a = static_cast<unsigned>(ga < cap_a ? ga : cap_a);
-    mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, 0, s>>>(S);
+    mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
     const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
     const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
     mvbk::vbyte_seg_decode<Delta, LL><<<grid_b, mvbk::kSegThreads, kSmemB, s>>>(S);
