@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem_a)) +
                           static_cast<uint32_t>((threadIdx.x >> 5) * kAStages * kSegASlice);
     if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane, ring);
+    // kernel B is launched as a programmatic dependent: it may start (and wait
+    // in griddepcontrol.wait) once every CTA of this grid got here
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Digit-weight sums of a lane's words: weight 1 after a terminator, 128
@@ -1366,6 +1369,9 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
     // the prefix); otherwise segments round-robin.
     const long long s0 = kLL ? gw * S.n_seg / nw : gw, s_step = kLL ? S.n_seg : nw;
     const long long s0_end = kLL ? (gw + 1) * S.n_seg / nw : 0;  // balanced runs: sizes differ by at most one
+    // kernel A's totals are complete and visible after this (a no-op unless
+    // launched as a programmatic dependent)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     for (long long s = s0; s < (kLL ? s0_end : S.n_seg); s += s_step) {
         const long long s_end = kLL ? s0_end : s + 1;

@@ -188,7 +188,19 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
     const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
     const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
-    mvbk::vbyte_seg_decode<Delta, LL><<<grid_b, mvbk::kSegThreads, kSmemB, s>>>(S);
+    // programmatic dependent launch: B's CTAs launch as A's retire and wait for A's
+    // results in griddepcontrol.wait (hides B's launch latency behind A's tail)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_b);
+    cfg.blockDim = dim3(mvbk::kSegThreads);
+    cfg.dynamicSmemBytes = kSmemB;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_seg_decode<Delta, LL>, S) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
