@@ -1,0 +1,172 @@
+"""Parity of the default lane-local decoder's distinct paths with the oracle:
+the fast path (1..4-byte integers, interior slices) against the general path
+(5-byte and malformed integers, range edges, the slice holding integer
+count-1), the swizzled staging layout of dense (mostly 1-byte) ranges, the
+16-byte (delta) and 32-byte (plain) lane widths, and kernel A's digit-weight
+segment sums with kernel B's straddle correction at every run start.  All
+comparisons bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import Oracle, STRICT
+from paper_1503_07387_b200 import mvb
+
+from test_decode_gpu import dev_decode, gpu_decode
+
+pytestmark = pytest.mark.gpu
+
+
+def _values_of_lengths(rng, lengths):
+    """One value per requested encoded length (1..5 bytes)."""
+    lo = np.array([0, 1 << 7, 1 << 14, 1 << 21, 1 << 28], np.uint64)
+    hi = np.array([1 << 7, 1 << 14, 1 << 21, 1 << 28, 1 << 32], np.uint64)
+    lengths = np.asarray(lengths)
+    return (lo[lengths - 1] + (rng.random(lengths.size) * (hi - lo)[lengths - 1]).astype(np.uint64)).astype(np.uint32)
+
+
+def _blocky_values(n, seed):
+    """Runs of 1-byte, 2-byte, 3..4-byte and 5-byte integers of random lengths
+    (dense ranges next to sparse ones, fast slices next to general ones)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    total = 0
+    while total < n:
+        kind = rng.integers(0, 5)
+        run = int(rng.integers(1, 4000))
+        if kind == 0:
+            lens = np.ones(run, np.int64)
+        elif kind == 1:
+            lens = rng.integers(1, 3, run)
+        elif kind == 2:
+            lens = rng.integers(3, 5, run)
+        elif kind == 3:
+            lens = np.full(run, 5)
+        else:
+            lens = rng.integers(1, 6, run)
+        out.append(_values_of_lengths(rng, lens))
+        total += run
+    return np.concatenate(out)[:n]
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return Oracle()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_blocky_streams_plain_and_delta(oracle, seed):
+    """Dense, sparse and mixed runs back to back: both lane widths, both
+    staging layouts, fast and general slices in one decode."""
+    v = _blocky_values(1_500_000, seed)
+    enc = oracle.encode_sequence(v)
+    ro, oo = oracle.decode(enc, v.size)
+    r, out = gpu_decode(enc, v.size)
+    assert r == ro and np.array_equal(out, oo)
+    ro, oo = oracle.decode_delta(enc, v.size, 12345)
+    r, out = gpu_decode(enc, v.size, delta=True, prev=12345)
+    assert r == ro and np.array_equal(out, oo)
+
+
+def test_delta_straddles_at_every_run_start(oracle):
+    """Only 3..5-byte integers: almost every segment (and so every warp run)
+    starts inside an integer, exercising the straddle correction of the
+    digit-weight segment sums."""
+    rng = np.random.default_rng(7)
+    v = _values_of_lengths(rng, rng.integers(3, 6, 2_000_000))
+    enc = oracle.encode_sequence(v)
+    ro, oo = oracle.decode_delta(enc, v.size, 0xFFFFFFF0)
+    r, out = gpu_decode(enc, v.size, delta=True, prev=0xFFFFFFF0)
+    assert r == ro and np.array_equal(out, oo)
+
+
+@pytest.mark.parametrize("delta", [False, True])
+def test_count_limits_inside_slices(oracle, delta):
+    """count below the stream's integer count, ending at many positions
+    inside 512-byte and 1 KiB slices (the general path's end-of-count)."""
+    rng = np.random.default_rng(11)
+    v = _values_of_lengths(rng, rng.integers(1, 3, 300_000))
+    enc = oracle.encode_sequence(v)
+    for count in (1, 2, 341, 342, 683, 1023, 1024, 1025, 4099, 150_001, 299_999):
+        if delta:
+            ro, oo = oracle.decode_delta(enc, count, 5)
+            r, out = gpu_decode(enc, count, delta=True, prev=5)
+        else:
+            ro, oo = oracle.decode(enc, count)
+            r, out = gpu_decode(enc, count)
+        assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (count, delta)
+
+
+@pytest.mark.parametrize("delta", [False, True])
+def test_dense_misaligned_with_guards(oracle, delta):
+    """All-1-byte data (swizzled staging) at every input and output
+    misalignment, with guard words around the output."""
+    import torch
+
+    cuda = torch.device("cuda", 0)
+    rng = np.random.default_rng(3)
+    v = rng.integers(0, 128, 70_001).astype(np.uint32)
+    enc = oracle.encode_sequence(v)
+    for in_off, out_off in ((0, 0), (1, 1), (7, 2), (15, 3), (8, 0)):
+        if delta:
+            ro, oo = oracle.decode_delta(enc, v.size, 99)
+        else:
+            ro, oo = oracle.decode(enc, v.size)
+        r, out = dev_decode(torch, cuda, enc, v.size, STRICT, delta, 99, in_off, out_off)
+        assert r == ro and np.array_equal(out, oo), (in_off, out_off, delta)
+
+
+def test_malformed_inside_dense_and_sparse_runs(oracle):
+    """A malformed run injected into dense data and into 5-byte data: the
+    first malformed integer's index and position, values before it."""
+    rng = np.random.default_rng(5)
+    for lens in (np.ones(200_000, np.int64), np.full(60_000, 5), rng.integers(1, 3, 150_000)):
+        v = _values_of_lengths(rng, lens)
+        enc = oracle.encode_sequence(v)
+        for pos in (100, 1023, 1024, 50_001, enc.size - 7):
+            bad = enc.copy()
+            bad[pos:pos + 6] = 0x80
+            for delta in (False, True):
+                if delta:
+                    ro, oo = oracle.decode_delta(bad, v.size, 1)
+                    r, out = gpu_decode(bad, v.size, delta=True, prev=1)
+                else:
+                    ro, oo = oracle.decode(bad, v.size)
+                    r, out = gpu_decode(bad, v.size)
+                assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (lens[0], pos, delta)
+
+
+@pytest.mark.parametrize("delta", [False, True])
+def test_lists_dense_and_sparse_around_slice_sizes(oracle, delta):
+    """Batched lists whose encoded sizes sit around 512 / 1024 / 2048 bytes,
+    dense (1-byte) and sparse (5-byte) ones interleaved."""
+    import torch
+
+    cuda = torch.device("cuda", 0)
+    rng = np.random.default_rng(13)
+    parts, counts = [], []
+    for l in range(400):
+        target = int(rng.choice([511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049, 3000]))
+        length = 1 if l % 2 else 5
+        n = max(1, target // length)
+        v = _values_of_lengths(rng, np.full(n, length))
+        parts.append(oracle.encode_sequence(v))
+        counts.append(n)
+    byte_off = np.zeros(len(parts) + 1, np.uint64)
+    byte_off[1:] = np.cumsum([p.size for p in parts])
+    int_off = np.zeros(len(parts) + 1, np.uint64)
+    int_off[1:] = np.cumsum(counts)
+    data = np.concatenate(parts)
+    prev = rng.integers(0, 1 << 32, len(parts), dtype=np.uint64).astype(np.uint32)
+    out = torch.full((int(int_off[-1]) + 4,), -1, dtype=torch.int32, device=cuda)
+    res = torch.zeros(len(parts) * 3, dtype=torch.int64, device=cuda)
+    d = mvb.Decoder(cuda, 1 << 16)
+    d.decode_lists(torch.from_numpy(data).to(cuda), torch.from_numpy(byte_off.view(np.int64)).to(cuda),
+                   torch.from_numpy(int_off.view(np.int64)).to(cuda), out,
+                   prev=torch.from_numpy(prev.view(np.int32)).to(cuda) if delta else None, results=res,
+                   delta=delta)
+    got = out.cpu().numpy().view(np.uint32)
+    rr = res.cpu().numpy().reshape(-1, 3)
+    for l, span in enumerate(parts):
+        ro, oo = oracle.decode_delta(span, counts[l], int(prev[l])) if delta else oracle.decode(span, counts[l])
+        assert tuple(int(x) for x in rr[l]) == tuple(ro), l
+        assert np.array_equal(got[int(int_off[l]):int(int_off[l + 1])], oo), l
