@@ -632,7 +632,8 @@ constexpr int kLLBlocksD = MVB_LL_BLOCKS_DELTA;    // (delta: the running sum an
 constexpr int kLLSlice = 1024;                     // bytes per slice: 32 lanes x 32 bytes
 constexpr int kLaneGroup = 2;                      // (V/EP-sized staging: 2 x 512 integers)
 constexpr int kLaneStage = kLaneGroup * 512 + 32;  // staging words per warp (+ alignment), whole 128-byte rows
-constexpr int kLaneWarpBytes = 4 * kLaneStage + 2 * kLLSlice;  // staging + 2-slice input ring
+constexpr int kLLWinBytes = 32 * 72;  // per warp: each lane's eight 8-byte digit windows (72-byte stride: 2 banks apart)
+constexpr int kLaneWarpBytes = 4 * kLaneStage + 2 * kLLSlice + kLLWinBytes;  // staging + 2-slice input ring + windows
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
 static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
 
@@ -1044,6 +1045,43 @@ __device__ __forceinline__ void gen_check_half(const ByteRange& R, long long q0,
     }
 }
 
+// Sparse general slices (plain decodes; few integers per lane, e.g. 5-byte
+// ones): instead of 32 static slots, one iteration per integer of the
+// busiest lane.  The lane's eight 56-bit digit windows (word k-1, word k) go
+// to shared memory; the integer ending at byte e has length 4 - (last
+// terminator among bytes e-4..e-1) (5 if none) and is read from window e / 4.
+template <bool kSwz>
+__device__ __forceinline__ void gen_sparse_plain(uint32_t wp3, const uint4 x0, const uint4 x1, uint32_t T32,
+                                                 uint32_t ends32, uint32_t sp, uint32_t win, uint32_t n_iter) {
+    const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    uint32_t cp = pack28(wp3);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t ck = pack28(w[k]);
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(win + 8u * k), "r"(cp + (ck << 28)), "r"(ck >> 4)
+                     : "memory");
+        cp = ck;
+    }
+    __syncwarp();
+    const uint32_t tlo = hibits4(~wp3) | (T32 << 4), thi = T32 >> 28;  // terminators, positions -4..31
+    uint32_t M = ends32;
+    for (uint32_t it = 0; it < n_iter; ++it) {
+        if (M) {
+            const uint32_t e = __ffs(M) - 1;
+            M &= M - 1;
+            const uint32_t nib = __funnelshift_r(tlo, thi, e) & 0xFu;  // terminators at bytes e-4..e-1
+            const uint32_t L = 3u - (31u - __clz(nib)) + 1u;           // 5 if none
+            uint2 wd;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(wd.x), "=r"(wd.y) : "r"(win + 8u * (e >> 2)) : "memory");
+            const uint32_t t = e & 3u;
+            const uint32_t top = __funnelshift_r(wd.x, wd.y, 3u + 7u * t);  // bits ending with byte e
+            const uint32_t v = L >= 5u ? __funnelshift_r(wd.x, wd.y, 7u * t) : __umulhi(top, 1u << (7u * L));
+            sts_stage<kSwz>(sp, v);
+            sp += 4;
+        }
+    }
+}
+
 // The general path of one slice (lane = 32 bytes w[0..7], as two 16-byte
 // halves): strict checks, then the general slots.  Delta: both halves' sums
 // first (the output order is lane-major), one warp scan, then the stores.
@@ -1051,7 +1089,7 @@ template <bool kDelta, bool kSwz>
 __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
                                           uint32_t wp2, uint32_t wp3, uint32_t T32, uint32_t inr32, uint32_t n_w,
                                           uint32_t wexcl, unsigned long long rs, unsigned long long limit,
-                                          const RangeSink& K, uint32_t sp, uint32_t& carry) {
+                                          const RangeSink& K, uint32_t sp, uint32_t win, uint32_t& carry) {
     const uint32_t e0 = T32 & inr32 & 0xFFFFu, e1 = (T32 & inr32) >> 16;
     gen_check_half(R, q0, x0.x, x0.y, x0.z, x0.w, wp2, wp3, T32 & 0xFFFFu, inr32 & 0xFFFFu, n_w, wexcl, rs, limit,
                    K);
@@ -1066,8 +1104,13 @@ __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, cons
         gen_half<2, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, sp, ex);
         gen_half<2, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, ex + s0);
     } else {
-        gen_half<1, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, sp, 0u);
-        gen_half<1, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, 0u);
+        const uint32_t n_iter = __reduce_max_sync(0xFFFFFFFFu, __popc(e0) + __popc(e1));
+        if (n_iter <= 10) {  // (at c1 density, 16-20 iterations, the static slots are faster)
+            gen_sparse_plain<kSwz>(wp3, x0, x1, T32, T32 & inr32, sp, win, n_iter);
+        } else {
+            gen_half<1, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, sp, 0u);
+            gen_half<1, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, 0u);
+        }
     }
 }
 
@@ -1200,7 +1243,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
         else
             ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
-                                       st_base + 4u * (a + wexcl), carry);
+                                       st_base + 4u * (a + wexcl), ring + 2u * kLLSlice + 72u * lane, carry);
         left = left > n_w ? left - n_w : 0u;
         if (n_w == 0) continue;
         __syncwarp();
