@@ -133,6 +133,19 @@ def set_kernel_choice(choice: int) -> None:
     f(int(choice))
 
 
+def set_host_pipeline(min_bytes: int = 4 << 20, chunk_bytes: int = 1 << 20, grow: bool = True) -> None:
+    """Testing switch (internal symbol mvbx_set_host_pipeline): the host
+    drop-ins (mvb_decode_stream / mvb_decode_delta_stream, strict mode) decode
+    streams of at least `min_bytes` scanned bytes in chunks (whole 32-segment
+    groups), the first of about `chunk_bytes`, later ones doubling up to 16 MB
+    if `grow`, overlapping H2D, decode and D2H; the defaults are the
+    library's."""
+    f = lib().mvbx_set_host_pipeline
+    f.argtypes = [ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int]
+    f.restype = None
+    f(int(min_bytes), int(chunk_bytes), int(bool(grow)))
+
+
 def workload_lib():
     """Host-side generators/encoder used to build bench and test inputs."""
     global _wlib

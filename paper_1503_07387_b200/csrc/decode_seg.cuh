@@ -62,6 +62,18 @@ struct SegParams {
     unsigned long long* gsum;
     WsHeader* hdr;
     mvb_result* res_dev;
+    // segments [s_lo, s_hi) of this launch pair (the whole stream, or one chunk
+    // of a pipelined host decode: group-aligned, chunks launched in order).  The
+    // integer count and value sum of the groups before s_lo come from base_in
+    // (null: zero); the last CTA of kernel B publishes those before s_hi to
+    // base_out (the next chunk's base_in) and chunk_total (host-mapped), and
+    // re-zeroes the launch's group accumulators.  Only the final launch
+    // produces the DecodeResult and resets the header.
+    long long s_lo, s_hi;
+    int final_launch;
+    const unsigned long long* base_in;         // [count, sum] of the groups before s_lo, or null
+    unsigned long long* base_out;              // non-final: [count, sum] of the groups before s_hi
+    volatile unsigned long long* chunk_total;  // non-final: integers ending in segments < s_hi
 };
 
 // Stream byte at aligned coordinate q (0x00 before the stream: the start is an
@@ -162,7 +174,8 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const long long s_begin = gw * S.n_seg / nw, s_end = (gw + 1) * S.n_seg / nw;  // balanced runs
+    const long long ns = S.s_hi - S.s_lo;
+    const long long s_begin = S.s_lo + gw * ns / nw, s_end = S.s_lo + (gw + 1) * ns / nw;  // balanced runs
     extern __shared__ __align__(128) uint8_t smem_a[];
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem_a)) +
                           static_cast<uint32_t>((threadIdx.x >> 5) * kAStages * kSegASlice);
@@ -1410,19 +1423,24 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
     // kLL: one contiguous run of segments per warp (the output index and carry
     // after segment s are those of s + 1, so only the run's first segment needs
     // the prefix); otherwise segments round-robin.
-    const long long s0 = kLL ? gw * S.n_seg / nw : gw, s_step = kLL ? S.n_seg : nw;
-    const long long s0_end = kLL ? (gw + 1) * S.n_seg / nw : 0;  // balanced runs: sizes differ by at most one
+    const long long ns = S.s_hi - S.s_lo;
+    const long long s0 = S.s_lo + (kLL ? gw * ns / nw : gw), s_step = kLL ? ns : nw;
+    const long long s0_end = kLL ? S.s_lo + (gw + 1) * ns / nw : 0;  // balanced runs: sizes differ by at most one
     // kernel A's totals are complete and visible after this (a no-op unless
     // launched as a programmatic dependent)
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    for (long long s = s0; s < (kLL ? s0_end : S.n_seg); s += s_step) {
+    for (long long s = s0; s < (kLL ? s0_end : S.s_hi); s += s_step) {
         const long long s_end = kLL ? s0_end : s + 1;
         // ---- output index and carry of the segment: groups before + segments before in the group ----
         unsigned long long base = 0;
         unsigned long long csum = 0;
         const long long g = s >> 5;
-        for (long long k = lane; k < g; k += 32) {
+        if (lane == 0 && S.base_in) {
+            base = S.base_in[0];
+            csum = S.base_in[1];
+        }
+        for (long long k = (S.s_lo >> 5) + lane; k < g; k += 32) {
             base += S.gcnt[k];
             if (kDelta) csum += S.gsum[k];
         }
@@ -1476,20 +1494,46 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // total integer count; then zero the group accumulators for the next launch
-    unsigned long long tot = 0;
-    for (long long k = threadIdx.x; k < S.n_grp; k += blockDim.x) tot += S.gcnt[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
-    __shared__ unsigned long long s_tot[kSegWarps];
-    if (lane == 0) s_tot[wid] = tot;
-    __syncthreads();
-    for (long long k = threadIdx.x; k < S.n_grp; k += blockDim.x) {
+    // integer count and value sum of the groups before s_hi; then zero this
+    // launch's group accumulators for the next launch
+    const long long g_lo = S.s_lo >> 5, g_hi = (S.s_hi + 31) >> 5;
+    unsigned long long tot = 0, tsum = 0;
+    for (long long k = g_lo + threadIdx.x; k < g_hi; k += blockDim.x) {
+        tot += S.gcnt[k];
+        tsum += S.gsum[k];
         S.gcnt[k] = 0;
         S.gsum[k] = 0;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+        tsum += __shfl_xor_sync(0xFFFFFFFFu, tsum, o);
+    }
+    __shared__ unsigned long long s_tot[kSegWarps], s_sum[kSegWarps];
+    if (lane == 0) {
+        s_tot[wid] = tot;
+        s_sum[wid] = tsum;
+    }
+    __syncthreads();
+    if (!S.final_launch) {  // a chunk of a pipelined decode: publish, keep the header
+        if (threadIdx.x == 0) {
+            unsigned long long total = S.base_in ? S.base_in[0] : 0ull, sum = S.base_in ? S.base_in[1] : 0ull;
+            for (int k = 0; k < kSegWarps; ++k) {
+                total += s_tot[k];
+                sum += s_sum[k];
+            }
+            S.base_out[0] = total;
+            S.base_out[1] = sum;
+            if (S.chunk_total) {
+                *S.chunk_total = total;
+                __threadfence_system();
+            }
+            S.hdr->done = 0;
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
-        unsigned long long total = 0;
+        unsigned long long total = S.base_in ? S.base_in[0] : 0ull;
         for (int k = 0; k < kSegWarps; ++k) total += s_tot[k];
         WsHeader* h = S.hdr;
         const unsigned long long err_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_idx_inv);

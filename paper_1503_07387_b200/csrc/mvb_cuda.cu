@@ -120,8 +120,19 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
 
 // Two-kernel segmented strict decode (decode_seg.cuh): group accumulators
 // zeroed, segment totals, then one warp per segment.
+//
+// seg_setup fills the launch parameters (segment size: about per_warp segments
+// per kernel-B warp over `plan_len` bytes -- the stream, or one chunk of a
+// pipelined host decode -- in whole kernel-A iterations); seg_launch_pair
+// launches kernel A and kernel B (a programmatic dependent of A) over the
+// segments [s_lo, s_hi).
+struct SegLaunch {
+    mvbk::SegParams S;
+    unsigned grid_a_cap, grid_b_cap;
+};
+
 template <bool Delta, int LL>
-int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cudaStream_t s, SegLaunch& sl) {
     constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
     static int per_sm = -1;
     int dev = 0;
@@ -138,20 +149,31 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
             return MVB_ERR_CUDA;
         per_sm = n > 0 ? n : 1;
     }
+    static int per_sm_a = -1;
+    if (per_sm_a < 0) {
+        int n = 0;
+        if (cudaFuncSetAttribute(mvbk::vbyte_seg_totals<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mvbk::kASmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads,
+                                                          mvbk::kASmem) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        per_sm_a = n > 0 ? n : 1;
+    }
     const long long ctas = static_cast<long long>(per_sm) * sms;
     const long long warps = ctas * mvbk::kSegWarps;
     const long long qlen = p.mis + p.len;
     // segments per kernel-B warp: LL decodes a balanced contiguous run of them per
     // warp (finer is better balanced), V/EP hands them out round-robin
     const long long per_warp = LL ? 8 : 4;
-    long long seg = (qlen + per_warp * warps - 1) / (per_warp * warps);
-    seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: 2 KiB slices
+    long long seg = (plan_len + per_warp * warps - 1) / (per_warp * warps);
+    seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: whole iterations
     if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
     const long long n_seg = (qlen + seg - 1) / seg;
     const long long n_grp = (n_seg + 31) / 32;
     const size_t need = kHeaderBytes + 8 * static_cast<size_t>(n_seg) + 16 * static_cast<size_t>(n_grp);
     if (ws_bytes < need) return MVB_ERR_WORKSPACE;
-    mvbk::SegParams S;
+    mvbk::SegParams& S = sl.S;
     S.in = p.in;
     S.mis = p.mis;
     S.len = p.len;
@@ -169,25 +191,36 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     S.ssum = S.scnt + n_seg;
     S.hdr = p.hdr;
     S.res_dev = p.res_dev;
+    S.s_lo = 0;
+    S.s_hi = n_seg;
+    S.final_launch = 1;
+    S.chunk_total = nullptr;
+    S.base_in = nullptr;
+    S.base_out = nullptr;
+    sl.grid_a_cap = static_cast<unsigned>(static_cast<long long>(per_sm_a) * sms);
+    sl.grid_b_cap = static_cast<unsigned>(ctas);
     if (prepare_workspace(ws, need, (4ull << 56) | static_cast<unsigned long long>(n_seg), s) != cudaSuccess)
         return MVB_ERR_CUDA;
-    static int per_sm_a = -1;
-    if (per_sm_a < 0) {
-        int n = 0;
-        if (cudaFuncSetAttribute(mvbk::vbyte_seg_totals<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kASmem) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads,
-                                                          mvbk::kASmem) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        per_sm_a = n > 0 ? n : 1;
-    }
-    const long long ga = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;  // at least one segment per warp
-    const long long cap_a = static_cast<long long>(per_sm_a) * sms;
-    const unsigned grid_a = static_cast<unsigned>(ga < cap_a ? ga : cap_a);
+    return 0;
+}
+
+template <bool Delta, int LL>
+int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_launch,
+                    volatile unsigned long long* chunk_total, const unsigned long long* base_in,
+                    unsigned long long* base_out, cudaStream_t s) {
+    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
+    mvbk::SegParams S = sl.S;
+    S.s_lo = s_lo;
+    S.s_hi = s_hi;
+    S.final_launch = final_launch ? 1 : 0;
+    S.chunk_total = chunk_total;
+    S.base_in = base_in;
+    S.base_out = base_out;
+    const long long n = s_hi - s_lo;
+    const long long ga = (n + mvbk::kSegWarps - 1) / mvbk::kSegWarps;  // at least one segment per warp
+    const unsigned grid_a = static_cast<unsigned>(ga < sl.grid_a_cap ? ga : sl.grid_a_cap);
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
-    const long long gb = (n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps;
-    const unsigned grid_b = static_cast<unsigned>(gb < ctas ? gb : ctas);
+    const unsigned grid_b = static_cast<unsigned>(ga < sl.grid_b_cap ? ga : sl.grid_b_cap);
     // programmatic dependent launch: B's CTAs launch as A's retire and wait for A's
     // results in griddepcontrol.wait (hides B's launch latency behind A's tail)
     cudaLaunchConfig_t cfg = {};
@@ -202,6 +235,14 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_seg_decode<Delta, LL>, S) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+template <bool Delta, int LL>
+int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+    SegLaunch sl;
+    const int rc = seg_setup<Delta, LL>(p, ws, ws_bytes, p.mis + p.len, s, sl);
+    if (rc) return rc;
+    return seg_launch_pair<Delta, LL>(sl, 0, sl.S.n_seg, true, nullptr, nullptr, nullptr, s);
 }
 
 // Persistent warp-sliced launch (decode_v3.cuh).
@@ -368,7 +409,8 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
 
 // Device buffers behind the synchronous host drop-ins, cached per thread.
 struct HostCtx {
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // pipelined decode: copies in each direction
     uint8_t* d_in = nullptr;
     size_t in_cap = 0;
     uint32_t* d_out = nullptr;
@@ -376,12 +418,38 @@ struct HostCtx {
     void* d_ws = nullptr;
     size_t ws_cap = 0;
     mvb_result* d_res = nullptr;
+    unsigned long long* d_base = nullptr;  // pipelined decode: [count, sum] before each chunk
+    // pinned, device-mapped: per-chunk integer totals and the DecodeResult the
+    // final kernel writes (read by the host once the kernel's event completed)
+    unsigned long long* h_tot = nullptr;
+    unsigned long long* dm_tot = nullptr;
+    mvb_result* h_res = nullptr;
+    mvb_result* dm_res = nullptr;
+    cudaEvent_t ev_in[64] = {}, ev_kst[64] = {}, ev_dec[64] = {}, ev_out[64] = {}, ev_start = nullptr;
+    int last_chunks = 0;  // chunks of the last pipelined call (mvbx_host_timeline)
     bool ok = false;
 
     bool init() {
         if (ok) return true;
-        if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess)
+            return false;
         if (cudaMalloc(&d_res, sizeof(mvb_result)) != cudaSuccess) return false;
+        if (cudaMalloc(&d_base, 2 * 65 * sizeof(unsigned long long)) != cudaSuccess) return false;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&h_tot), 64 * sizeof(unsigned long long), cudaHostAllocMapped) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&dm_tot), h_tot, 0) != cudaSuccess)
+            return false;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&h_res), sizeof(mvb_result), cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&dm_res), h_res, 0) != cudaSuccess)
+            return false;
+        for (int i = 0; i < 64; ++i)
+            if (cudaEventCreate(&ev_in[i]) != cudaSuccess || cudaEventCreate(&ev_dec[i]) != cudaSuccess ||
+                cudaEventCreate(&ev_kst[i]) != cudaSuccess ||
+                cudaEventCreate(&ev_out[i]) != cudaSuccess)
+                return false;
+        if (cudaEventCreate(&ev_start) != cudaSuccess) return false;
         ok = true;
         return true;
     }
@@ -401,6 +469,114 @@ struct HostCtx {
 
 thread_local HostCtx g_ctx;
 
+// Pipelined host decode (strict mode, segmented kernels): the scanned bytes are
+// cut into group-aligned chunks.  All H2D copies are queued on one stream;
+// chunk c's kernel pair waits for its copy (it reads no byte after the chunk)
+// and decodes the integers ending in it; once it completes, the host reads the
+// integers ending before the chunk's end (published by the kernel into mapped
+// memory) and queues the D2H of that output range on a third stream.  PCIe is
+// full duplex, so the input of later chunks, the decode and the output of
+// earlier chunks overlap: a call costs about max(H2D, D2H) instead of their sum.
+size_t g_pipe_min = 4u << 20;     // scanned bytes from which the host drop-in pipelines
+size_t g_pipe_chunk = 1u << 20;   // bytes of the first chunk (later ones double, up to 16 MB; at most 64)
+bool g_pipe_grow = true;          // (tests: false keeps every chunk at g_pipe_chunk)
+
+template <bool Delta>
+int decode_host_pipelined(HostCtx& c, const uint8_t* in, size_t scan, size_t count, uint32_t prev, uint32_t* out,
+                          mvb_result* res) {
+    Params p = {};
+    p.in = c.d_in;
+    p.mis = 0;  // cudaMalloc'd: aligned
+    p.len = static_cast<long long>(scan);
+    p.count = count;
+    p.out = c.d_out;
+    p.prev = prev;
+    p.prev_dev = nullptr;
+    p.hdr = static_cast<WsHeader*>(c.d_ws);
+    // the kernels write the chunk totals and the DecodeResult straight into
+    // mapped host memory (a small D2H copy would queue behind the output copies)
+    p.res_dev = c.dm_res;
+    SegLaunch sl;
+    int rc = seg_setup<Delta, 1>(p, c.d_ws, c.ws_cap, static_cast<long long>(std::min(scan, g_pipe_chunk)), c.stream,
+                                 sl);
+    if (rc) return rc;
+    // chunk k covers segments [cb[k], cb[k + 1]): whole groups, the first of about
+    // g_pipe_chunk bytes, each next one larger by `growth` (up to 16 MB), so the
+    // D2H queue stays fed while the pipeline fill is one small chunk; at most 64
+    // chunks
+    const long long seg = sl.S.seg_bytes, n_seg = sl.S.n_seg;
+    long long cb[65];
+    int n_chunks = 0;
+    {
+        // growth factor: the next chunk's input should arrive (H2D) no later than
+        // this chunk's output leaves (D2H), i.e. about the output/input byte ratio
+        // (both directions move ~55 GB/s), between 1 and 2
+        const double growth =
+            g_pipe_grow ? std::min(2.0, std::max(1.0, 0.9 * 4.0 * static_cast<double>(count) / scan)) : 1.0;
+        long long grp0 = (static_cast<long long>(g_pipe_chunk) + 32 * seg - 1) / (32 * seg);
+        if (grp0 < 1) grp0 = 1;
+        for (;;) {  // (a larger first chunk until the schedule fits 64 chunks)
+            const long long cap = std::max<long long>(grp0, (16ll << 20) / (32 * seg));
+            long long grp = grp0, at = 0;
+            n_chunks = 0;
+            cb[0] = 0;
+            while (at < n_seg && n_chunks < 64) {
+                at = std::min(n_seg, at + 32 * grp);
+                cb[++n_chunks] = at;
+                grp = std::min<long long>(cap, std::max<long long>(grp, static_cast<long long>(grp * growth)));
+            }
+            if (at >= n_seg) break;
+            grp0 *= 2;
+        }
+    }
+    // host-side order keeps the API calls off the critical path: chunk 0's copy
+    // and kernels first, then the other copies, then one chunk's kernels ahead
+    // of each D2H the host waits for
+    auto h2d = [&](int k) -> bool {
+        const size_t b0 = static_cast<size_t>(cb[k] * seg);
+        const size_t b1 = std::min(scan, static_cast<size_t>(cb[k + 1] * seg));
+        if (b1 > b0 && cudaMemcpyAsync(c.d_in + b0, in + b0, b1 - b0, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
+            return false;
+        return cudaEventRecord(c.ev_in[k], c.h2d) == cudaSuccess;
+    };
+    auto kernels = [&](int k) -> int {
+        if (cudaStreamWaitEvent(c.stream, c.ev_in[k], 0) != cudaSuccess) return MVB_ERR_CUDA;
+        if (cudaEventRecord(c.ev_kst[k], c.stream) != cudaSuccess) return MVB_ERR_CUDA;
+        const int e = seg_launch_pair<Delta, 1>(sl, cb[k], cb[k + 1], k == n_chunks - 1, c.dm_tot + k,
+                                                k ? c.d_base + 2 * k : nullptr, c.d_base + 2 * (k + 1), c.stream);
+        if (e) return e;
+        return cudaEventRecord(c.ev_dec[k], c.stream) == cudaSuccess ? 0 : MVB_ERR_CUDA;
+    };
+    if (cudaEventRecord(c.ev_start, c.h2d) != cudaSuccess) return MVB_ERR_CUDA;
+    c.last_chunks = n_chunks;
+    if (!h2d(0)) return MVB_ERR_CUDA;
+    if ((rc = kernels(0)) != 0) return rc;
+    for (int k = 1; k < n_chunks; ++k)
+        if (!h2d(k)) return MVB_ERR_CUDA;
+    size_t done = 0;
+    mvb_result r = {};
+    for (int k = 0; k < n_chunks; ++k) {
+        if (k + 1 < n_chunks && (rc = kernels(k + 1)) != 0) return rc;
+        if (cudaEventSynchronize(c.ev_dec[k]) != cudaSuccess) return MVB_ERR_CUDA;
+        size_t upto;
+        if (k < n_chunks - 1) {
+            const unsigned long long t = static_cast<volatile unsigned long long*>(c.h_tot)[k];
+            upto = static_cast<size_t>(t < count ? t : count);
+        } else {
+            r = *const_cast<const mvb_result*>(static_cast<volatile mvb_result*>(c.h_res));
+            upto = std::max(done, static_cast<size_t>(r.values_written));
+        }
+        if (upto > done && cudaMemcpyAsync(out + done, c.d_out + done, (upto - done) * 4, cudaMemcpyDeviceToHost,
+                                           c.d2h) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        done = upto > done ? upto : done;
+        if (cudaEventRecord(c.ev_out[k], c.d2h) != cudaSuccess) return MVB_ERR_CUDA;
+    }
+    if (cudaStreamSynchronize(c.d2h) != cudaSuccess) return MVB_ERR_CUDA;
+    if (res) *res = r;
+    return r.status;
+}
+
 int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev, uint32_t* out,
                 int mode, mvb_result* res) {
     if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
@@ -408,10 +584,14 @@ int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint
     HostCtx& c = g_ctx;
     if (!c.init()) return MVB_ERR_CUDA;
     const size_t scan = scan_length(in_len, count);
-    const size_t wsb = mvb_workspace_bytes(scan);
+    // the pipelined decode's segments can be finer than the one-shot decode's
+    const size_t wsb = std::max(mvb_workspace_bytes(scan), kHeaderBytes + 9 * (scan / 1024 + 2) + 64);
     if (!HostCtx::grow(c.d_in, c.in_cap, scan, false) || !HostCtx::grow(c.d_out, c.out_cap, count * 4, false) ||
         !HostCtx::grow(c.d_ws, c.ws_cap, wsb, true))
         return MVB_ERR_CUDA;
+    if (mode == MVB_STRICT && g_kernel_choice == 0 && count > 0 && scan >= g_pipe_min)
+        return delta ? decode_host_pipelined<true>(c, in, scan, count, prev, out, res)
+                     : decode_host_pipelined<false>(c, in, scan, count, prev, out, res);
     if (scan && cudaMemcpyAsync(c.d_in, in, scan, cudaMemcpyHostToDevice, c.stream) != cudaSuccess)
         return MVB_ERR_CUDA;
     const int rc = decode_device(scan ? c.d_in : nullptr, scan, count, delta, prev, count ? c.d_out : nullptr,
@@ -665,6 +845,32 @@ int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta
 
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
+
+// Internal profiling entry (not part of include/mvb_cuda.h): the calling
+// thread's last pipelined host decode as t[4k + {0,1,2,3}] = ms from its start
+// to the end of chunk k's H2D, the start and end of its kernels and the end of
+// its D2H; returns the chunk count.
+int mvbx_host_timeline(float* t, int cap) {
+    HostCtx& c = g_ctx;
+    if (!c.ok || c.last_chunks == 0) return 0;
+    const int n = c.last_chunks < cap ? c.last_chunks : cap;
+    for (int k = 0; k < n; ++k) {
+        cudaEventElapsedTime(&t[4 * k], c.ev_start, c.ev_in[k]);
+        cudaEventElapsedTime(&t[4 * k + 1], c.ev_start, c.ev_kst[k]);
+        cudaEventElapsedTime(&t[4 * k + 2], c.ev_start, c.ev_dec[k]);
+        cudaEventElapsedTime(&t[4 * k + 3], c.ev_start, c.ev_out[k]);
+    }
+    return c.last_chunks;
+}
+
+// Internal testing switch (not part of include/mvb_cuda.h): the scanned size
+// from which the host drop-ins pipeline, their first chunk's bytes, and whether
+// later chunks double.
+void mvbx_set_host_pipeline(size_t min_bytes, size_t chunk_bytes, int grow) {
+    g_pipe_min = min_bytes;
+    g_pipe_chunk = chunk_bytes ? chunk_bytes : 1;
+    g_pipe_grow = grow != 0;
+}
 
 // Kernels one decode call launches in steady state (bench accounting; the
 // workspace re-zeroing memset runs only when a workspace changes layout).
