@@ -36,6 +36,13 @@
 
 namespace mvbk {
 
+#ifndef MVB_TRACE_B
+#define MVB_TRACE_B 0  // 1: kernel B records per-warp timestamps (profiling builds only)
+#endif
+#if MVB_TRACE_B
+__device__ unsigned long long* mvb_trace_b;  // 6 words per warp: start, after wait, after prefix, end, segments, SM
+#endif
+
 constexpr int kSegWarps = 4;  // warps per CTA
 constexpr int kSegThreads = 32 * kSegWarps;
 constexpr int kSegSlice = 512;
@@ -60,6 +67,9 @@ struct SegParams {
     uint32_t* ssum;       // per-segment value sum mod 2^32
     unsigned long long* gcnt;  // per-group sums of scnt / ssum (zeroed by the finalizing CTA)
     unsigned long long* gsum;
+    unsigned long long* ucnt;  // per-supergroup (32 groups) sums of gcnt / gsum (zeroed likewise)
+    unsigned long long* usum;
+    long long n_sup;           // ceil(n_grp / 32)
     WsHeader* hdr;
     mvb_result* res_dev;
     // segments [s_lo, s_hi) of this launch pair (the whole stream, or one chunk
@@ -262,6 +272,7 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
     unsigned cnt = 0;
     uint32_t sum = 0;
     unsigned long long gc = 0, gs = 0;  // totals of the run's segments in the current group
+    unsigned long long uc = 0, us = 0;  // ... in the current supergroup
     long long s = s_begin;
     int it_s = 0;  // iteration within segment s
     for (int it = 0; it < n_it; ++it) {
@@ -334,8 +345,18 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
                     atomicAdd(S.gcnt + (s >> 5), gc);
                     if (kDelta) atomicAdd(S.gsum + (s >> 5), gs);
                 }
+                uc += gc;
+                us += gs;
                 gc = 0;
                 gs = 0;
+                if (((s + 1) & 1023) == 0 || s + 1 == s_end) {  // supergroup accumulators (32 groups)
+                    if (lane == 0) {
+                        atomicAdd(S.ucnt + (s >> 10), uc);
+                        if (kDelta) atomicAdd(S.usum + (s >> 10), us);
+                    }
+                    uc = 0;
+                    us = 0;
+                }
             }
             cnt = 0;
             sum = 0;
@@ -780,6 +801,87 @@ __device__ __forceinline__ void lane_slots_fast16(uint32_t wp3, uint32_t w0, uin
             else
                 MVB_SLOT_PLAIN("@p st.shared.u32 [%0], t;\n\t");
 #undef MVB_SLOT_PLAIN
+        }
+    }
+}
+
+// Slots of a slice whose integers all have 1 or 2 bytes (no two consecutive
+// continuation bytes in the lane's bytes and the one before them; every
+// integer is inside the range): the integer ending at byte t of word k is
+//   d(t)                       if byte t-1 is a terminator,
+//   d(t-1) | d(t) << 7         if byte t-1 is a continuation byte,
+// d = 7-bit digit.  Per word, SWAR builds A (low byte of each candidate:
+// d(t), or d(t-1) with bit 0 of d(t) at bit 7) and B (high byte: d(t) >> 1,
+// or 0); the candidate of byte t is then one prmt of A and B (bytes 2..3
+// replicate the sign of B's byte, which is 0).  Per slot: prmt, the
+// terminator predicate, the (running sum and) store, the pointer bump.
+// Delta: the lane's integer sum is two dp4a per word over the terminator
+// bytes (its integers are complete: an integer straddling into the lane is
+// built from the previous lane's last byte), then the warp scan.
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+template <bool kDelta, bool kSwz, int NW>
+__device__ __forceinline__ void lane_slots_2b(uint32_t wp3, const uint32_t (&w)[NW], uint32_t T, uint32_t sp,
+                                              uint32_t& carry) {
+    uint32_t A[NW], B[NW];
+    uint32_t own = 0, prev = wp3;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const uint32_t P = __funnelshift_l(prev, w[k], 8);  // byte t = byte t-1 of the stream
+        const uint32_t cm = ((P >> 7) & 0x01010101u) * 0xFFu;  // 0xFF where byte t-1 continues
+        const uint32_t X = (P & 0x7F7F7F7Fu) | ((w[k] << 7) & 0x80808080u);
+        A[k] = (X & cm) | (w[k] & ~cm);
+        B[k] = (w[k] >> 1) & 0x3F3F3F3Fu & cm;
+        if (kDelta) {
+            const uint32_t tm = (~w[k] >> 7) & 0x01010101u;  // terminator bytes
+            own = __dp4a(A[k], tm, own);
+            own += __dp4a(B[k], tm, 0u) << 8;
+        }
+        prev = w[k];
+    }
+    uint32_t acc = 0;
+    if (kDelta) acc = lane_scan_offset<kDelta>(own, carry);
+#pragma unroll
+    for (int e = 0; e < 4 * NW; ++e) {
+        const int k = e >> 2, t = e & 3;
+        const uint32_t sel = static_cast<uint32_t>(t | ((4 + t) << 4) | ((12 + t) << 8) | ((12 + t) << 12));
+        const uint32_t v = prmt_sign(A[k], B[k], sel);
+        if (kDelta) {
+#define MVB_SLOT2_DELTA(STORE)                                                         \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
+                 "and.b32 t, %2, %4;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "@p add.u32 %1, %1, %3;\n\t" STORE                                      \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(acc)                                                      \
+                 : "r"(T), "r"(v), "r"(1u << e)                                             \
+                 : "memory")
+            if (kSwz)
+                MVB_SLOT2_DELTA("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
+                                "@p st.shared.u32 [t], %1;\n\t");
+            else
+                MVB_SLOT2_DELTA("@p st.shared.u32 [%0], %1;\n\t");
+#undef MVB_SLOT2_DELTA
+        } else {
+#define MVB_SLOT2_PLAIN(STORE)                                                         \
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
+                 "and.b32 t, %1, %3;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t" STORE                                        \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "}"                                                                        \
+                 : "+r"(sp)                                                                 \
+                 : "r"(T), "r"(v), "r"(1u << e)                                             \
+                 : "memory")
+            if (kSwz)
+                MVB_SLOT2_PLAIN("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
+                                "@p st.shared.u32 [t], %2;\n\t");
+            else
+                MVB_SLOT2_PLAIN("@p st.shared.u32 [%0], %2;\n\t");
+#undef MVB_SLOT2_PLAIN
         }
     }
 }
@@ -1249,10 +1351,15 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         const uint32_t wexcl = incl - n_own;
         // four continuation bytes in a row anywhere in positions -4..31
         const unsigned long long C = ((static_cast<unsigned long long>(~T32) << 4) | (~hibits4(~wp3) & 0xFu));
-        const unsigned long long run4 = C & (C >> 1) & (C >> 2) & (C >> 3) & 0x1FFFFFFFFull;
-        const bool fast = !__any_sync(0xFFFFFFFFu, run4 != 0) && inter && n_w < left;
+        const unsigned long long pair = C & (C >> 1);                       // bit j: positions j-4, j-3 continue
+        const unsigned long long run2 = pair & 0xFFFFFFFFCull;              // a 3+-byte integer ends in 0..31
+        const unsigned long long run4 = pair & (pair >> 2) & 0x1FFFFFFFFull;  // a 5+-byte integer ends in 0..31
+        const bool ok_range = inter && n_w < left;
+        const unsigned vote = __ballot_sync(0xFFFFFFFFu, run2 != 0) | (__ballot_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
         if (n_w) last_i = i;
-        if (fast)
+        if (ok_range && vote == 0)
+            lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+        else if (ok_range && !(vote & 2u))
             lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
         else
             ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
@@ -1360,10 +1467,16 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
             const uint32_t wexcl = incl - n_own;
             const uint32_t C20 = ~(hibits4(~wp3) | (T16 << 4)) & 0xFFFFFu;  // continuation bytes, positions -4..15
-            const uint32_t run4 = C20 & (C20 >> 1) & (C20 >> 2) & (C20 >> 3);
-            const bool fast = !__any_sync(0xFFFFFFFFu, run4) && inter && n_w < left;
+            const uint32_t pair = C20 & (C20 >> 1);  // bit j: positions j-4, j-3 both continue
+            const uint32_t run2 = pair & 0xFFFFCu;     // a 3+-byte integer ends in 0..15
+            const uint32_t run4 = pair & (pair >> 2);  // a 5+-byte integer ends in 0..15
+            const bool ok_range = inter && n_w < left;
+            const unsigned vote = __ballot_sync(0xFFFFFFFFu, run2 != 0) | (__ballot_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
             if (n_w) last_i = i;
-            if (fast)
+            if (ok_range && vote == 0) {
+                const uint32_t wv[4] = {w0, w1, w2, w3};
+                lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16, st_base + 4u * (a + n_g + wexcl), carry);
+            } else if (ok_range && !(vote & 2u))
                 lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
             else
                 ll_slice_gen16<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3,
@@ -1407,85 +1520,20 @@ __device__ __forceinline__ void decode_range_llw(const ByteRange& R, long long q
     else decode_range_ll<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
 }
 
-// kLL: 0 decode_range (V / EP windows), 1 decode_range_ll (lane-local)
-template <bool kDelta, int kLL>
-__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 8) vbyte_seg_decode(SegParams S) {
-    extern __shared__ __align__(128) uint8_t smem[];
+// Completion of a kernel-B launch (all threads of every CTA call it): the
+// last CTA to arrive sums the launch's group totals and re-zeroes the
+// launch's group / supergroup accumulators; a non-final launch of a pipelined
+// decode publishes the totals before s_hi, the final one produces the
+// DecodeResult and resets the header.  find_last_end: the end of the stream's
+// last integer (needed only for a truncated stream) is found here -- the last
+// segment with an integer, then its last terminator byte -- instead of being
+// tracked by every range decode.
+template <int kNW>
+__device__ __forceinline__ void seg_complete(const SegParams& S, bool find_last_end) {
     __shared__ bool s_last;
-    const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
-    uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
-    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
-    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
-    // kLL: one contiguous run of segments per warp (the output index and carry
-    // after segment s are those of s + 1, so only the run's first segment needs
-    // the prefix); otherwise segments round-robin.
-    const long long ns = S.s_hi - S.s_lo;
-    const long long s0 = S.s_lo + (kLL ? gw * ns / nw : gw), s_step = kLL ? ns : nw;
-    const long long s0_end = kLL ? S.s_lo + (gw + 1) * ns / nw : 0;  // balanced runs: sizes differ by at most one
-    // kernel A's totals are complete and visible after this (a no-op unless
-    // launched as a programmatic dependent)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-
-    for (long long s = s0; s < (kLL ? s0_end : S.s_hi); s += s_step) {
-        const long long s_end = kLL ? s0_end : s + 1;
-        // ---- output index and carry of the segment: groups before + segments before in the group ----
-        unsigned long long base = 0;
-        unsigned long long csum = 0;
-        const long long g = s >> 5;
-        if (lane == 0 && S.base_in) {
-            base = S.base_in[0];
-            csum = S.base_in[1];
-        }
-        for (long long k = (S.s_lo >> 5) + lane; k < g; k += 32) {
-            base += S.gcnt[k];
-            if (kDelta) csum += S.gsum[k];
-        }
-        if (lane < (s & 31)) {
-            base += S.scnt[(g << 5) + lane];
-            if (kDelta) csum += S.ssum[(g << 5) + lane];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            base += __shfl_xor_sync(0xFFFFFFFFu, base, o);
-            if (kDelta) csum += __shfl_xor_sync(0xFFFFFFFFu, csum, o);
-        }
-        if (base >= S.count) continue;  // nothing of this segment is stored (warp-uniform)
-        // segment sums are digit-weight sums of the segments' bytes: the bytes before
-        // this segment that belong to the integer straddling its start (the partial
-        // value of the <= 4 bytes after the last terminator before it) are not yet
-        // an integer of the prefix
-        uint32_t straddle = 0;
-        if (kDelta) {
-            const uint32_t wb = r_word(R, s * S.seg_bytes - 4);
-            straddle = shr_clamp(pack28(wb), 7 * (32 - __clz(static_cast<int>(hibits4(~wb)))));
-        }
-        const uint32_t carry =
-            kDelta ? static_cast<uint32_t>(csum) - straddle + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
-        RangeOut ro;
-        const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
-        if (kLL) {
-            // integers in the run (segments s .. s_end - 1, at most 32 when kLL): its density
-            unsigned long long rc = (s + lane < s_end) ? S.scnt[s + lane] : 0u;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
-            if (range_dense(rc, (s_end - s) * S.seg_bytes))
-                decode_range_llw<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
-                                              reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
-            else
-                decode_range_llw<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
-                                               reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
-        }
-        else
-            decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
-                                 lane, K, ro);
-        if (lane == 0 && ro.last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
-    }
-
-    // ---- completion; the last CTA produces the DecodeResult ----
+    __shared__ unsigned long long s_tot[kNW], s_sum[kNW];
+    __shared__ long long s_seg;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1504,24 +1552,30 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
         S.gcnt[k] = 0;
         S.gsum[k] = 0;
     }
+    // supergroups the launch touched (one straddling two chunks of a pipelined
+    // decode is never read whole; both launches zero it)
+    for (long long k = (g_lo >> 5) + threadIdx.x; k < ((g_hi + 31) >> 5); k += blockDim.x) {
+        S.ucnt[k] = 0;
+        S.usum[k] = 0;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
         tsum += __shfl_xor_sync(0xFFFFFFFFu, tsum, o);
     }
-    __shared__ unsigned long long s_tot[kSegWarps], s_sum[kSegWarps];
     if (lane == 0) {
         s_tot[wid] = tot;
         s_sum[wid] = tsum;
     }
+    if (threadIdx.x == 0) s_seg = -1;
     __syncthreads();
+    unsigned long long total = S.base_in ? S.base_in[0] : 0ull, sum = S.base_in ? S.base_in[1] : 0ull;
+    for (int k = 0; k < kNW; ++k) {
+        total += s_tot[k];
+        sum += s_sum[k];
+    }
     if (!S.final_launch) {  // a chunk of a pipelined decode: publish, keep the header
         if (threadIdx.x == 0) {
-            unsigned long long total = S.base_in ? S.base_in[0] : 0ull, sum = S.base_in ? S.base_in[1] : 0ull;
-            for (int k = 0; k < kSegWarps; ++k) {
-                total += s_tot[k];
-                sum += s_sum[k];
-            }
             S.base_out[0] = total;
             S.base_out[1] = sum;
             if (S.chunk_total) {
@@ -1529,16 +1583,40 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
                 __threadfence_system();
             }
             S.hdr->done = 0;
+            S.hdr->ticket = 0;
         }
         return;
     }
+    WsHeader* h = S.hdr;
+    const unsigned long long err_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_idx_inv);
+    const bool truncated = !(err_inv != 0ull && ~err_inv < S.count) && total < S.count;  // (CTA-uniform)
+    long long last_end_found = 0;
+    if (find_last_end && truncated) {
+        for (long long hi = S.n_seg - 1; hi >= 0; hi -= blockDim.x) {
+            const long long k = hi - static_cast<long long>(threadIdx.x);
+            if (k >= 0 && S.scnt[k] > 0) atomicMax(&s_seg, k);
+            __syncthreads();
+            if (s_seg >= 0) break;
+        }
+        if (s_seg >= 0 && wid == 0) {
+            long long le = -1;
+            for (long long q = s_seg * S.seg_bytes + lane; q < (s_seg + 1) * S.seg_bytes; q += 32) {
+                const long long p = q - S.mis;
+                if (p >= 0 && p < S.len && S.in[p] < 0x80u) le = p + 1;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const long long x = __shfl_xor_sync(0xFFFFFFFFu, le, o);
+                le = x > le ? x : le;
+            }
+            last_end_found = le > 0 ? le : 0;
+        }
+    }
     if (threadIdx.x == 0) {
-        unsigned long long total = S.base_in ? S.base_in[0] : 0ull;
-        for (int k = 0; k < kSegWarps; ++k) total += s_tot[k];
-        WsHeader* h = S.hdr;
-        const unsigned long long err_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_idx_inv);
         const unsigned long long errpos_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_pos_inv);
-        const unsigned long long last_end = *reinterpret_cast<volatile unsigned long long*>(&h->last_end);
+        const unsigned long long last_end =
+            find_last_end ? static_cast<unsigned long long>(last_end_found)
+                          : *reinterpret_cast<volatile unsigned long long*>(&h->last_end);
         const unsigned long long count_end = *reinterpret_cast<volatile unsigned long long*>(&h->count_end);
         mvb_result r;
         r.reserved = 0;
@@ -1558,6 +1636,7 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
         h->result = r;
         if (S.res_dev) *S.res_dev = r;
         h->done = 0;
+        h->ticket = 0;
         h->err_idx_inv = 0;
         h->err_pos_inv = 0;
         h->last_end = 0;
@@ -1565,6 +1644,139 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
         h->epoch = h->epoch + 1;
     }
     __threadfence();
+}
+
+// Integer count and digit-weight sum of the stream before segment s (all
+// lanes get them): the launch's base, whole supergroups and the partial
+// groups at both ends of [g_lo, g), the segments before s in its group --
+// independent loads, one memory latency.
+template <bool kDelta>
+__device__ __forceinline__ void seg_prefix(const SegParams& S, long long s, int lane, unsigned long long& base,
+                                           unsigned long long& csum) {
+    base = 0;
+    csum = 0;
+    const long long g = s >> 5, g_lo = S.s_lo >> 5;
+    if (lane == 0 && S.base_in) {
+        base = S.base_in[0];
+        csum = S.base_in[1];
+    }
+    const long long ua = (g_lo + 31) >> 5, ub = g >> 5;  // whole supergroups [ua, ub)
+    if (ua < ub) {
+        const long long h = g_lo + lane, t = (ub << 5) + lane;
+        if (h < (ua << 5)) {
+            base += S.gcnt[h];
+            if (kDelta) csum += S.gsum[h];
+        }
+        if (t < g) {
+            base += S.gcnt[t];
+            if (kDelta) csum += S.gsum[t];
+        }
+        for (long long k = ua + lane; k < ub; k += 32) {
+            base += S.ucnt[k];
+            if (kDelta) csum += S.usum[k];
+        }
+    } else {
+        for (long long k = g_lo + lane; k < g; k += 32) {
+            base += S.gcnt[k];
+            if (kDelta) csum += S.gsum[k];
+        }
+    }
+    if (lane < (s & 31)) {
+        base += S.scnt[(g << 5) + lane];
+        if (kDelta) csum += S.ssum[(g << 5) + lane];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        base += __shfl_xor_sync(0xFFFFFFFFu, base, o);
+        if (kDelta) csum += __shfl_xor_sync(0xFFFFFFFFu, csum, o);
+    }
+}
+
+// kLL: 0 decode_range (V / EP windows), 1 decode_range_ll (lane-local)
+template <bool kDelta, int kLL>
+__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 8) vbyte_seg_decode(SegParams S) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
+    uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
+    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
+    // kLL: one contiguous run of segments per warp (the output index and carry
+    // after segment s are those of s + 1, so only the run's first segment needs
+    // the prefix); otherwise segments round-robin.
+    const long long ns = S.s_hi - S.s_lo;
+    const long long s0 = S.s_lo + (kLL ? gw * ns / nw : gw), s_step = kLL ? ns : nw;
+    const long long s0_end = kLL ? S.s_lo + (gw + 1) * ns / nw : 0;  // balanced runs: sizes differ by at most one
+    // kernel A's totals are complete and visible after this (a no-op unless
+    // launched as a programmatic dependent)
+#if MVB_TRACE_B
+    unsigned long long t_trace[4];
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[0]));
+#endif
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#if MVB_TRACE_B
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[1]));
+#endif
+
+    for (long long s = s0; s < (kLL ? s0_end : S.s_hi); s += s_step) {
+        const long long s_end = kLL ? s0_end : s + 1;
+        // ---- output index and carry of the segment ----
+        unsigned long long base, csum;
+        seg_prefix<kDelta>(S, s, lane, base, csum);
+        if (base >= S.count) continue;  // nothing of this segment is stored (warp-uniform)
+        // segment sums are digit-weight sums of the segments' bytes: the bytes before
+        // this segment that belong to the integer straddling its start (the partial
+        // value of the <= 4 bytes after the last terminator before it) are not yet
+        // an integer of the prefix
+        uint32_t straddle = 0;
+        if (kDelta) {
+            const uint32_t wb = r_word(R, s * S.seg_bytes - 4);
+            straddle = shr_clamp(pack28(wb), 7 * (32 - __clz(static_cast<int>(hibits4(~wb)))));
+        }
+        const uint32_t carry =
+            kDelta ? static_cast<uint32_t>(csum) - straddle + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
+        RangeOut ro;
+        const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
+#if MVB_TRACE_B
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[2]));
+#endif
+        if (kLL) {
+            // integers in the run (segments s .. s_end - 1, at most 32 when kLL): its density
+            unsigned long long rc = (s + lane < s_end) ? S.scnt[s + lane] : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
+            if (range_dense(rc, (s_end - s) * S.seg_bytes))
+                decode_range_llw<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                                              reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+            else
+                decode_range_llw<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                                               reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
+        }
+        else
+            decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
+                                 lane, K, ro);
+        if (lane == 0 && ro.last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
+    }
+#if MVB_TRACE_B
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[3]));
+    if (lane == 0 && mvb_trace_b) {
+        unsigned long long* t = mvb_trace_b + 6 * gw;
+        t[0] = t_trace[0];
+        t[1] = t_trace[1];
+        t[2] = t_trace[2];
+        t[3] = t_trace[3];
+        t[4] = static_cast<unsigned long long>(s0_end - s0);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        t[5] = smid;
+    }
+#endif
+
+    // ---- completion; the last CTA produces the DecodeResult ----
+    seg_complete<kSegWarps>(S, false);
 }
 
 // ------------------------------------------------------------------ batched lists

@@ -131,20 +131,28 @@ struct SegLaunch {
     unsigned grid_a_cap, grid_b_cap;
 };
 
+// LL: 0 V/EP range decode (choice 5), 1 lane-local (choice 0, default).
+template <int LL>
+constexpr int seg_b_smem() { return LL ? mvbk::kLaneSmem : mvbk::kSegSmem; }
+template <int LL>
+constexpr int seg_b_threads() { return mvbk::kSegThreads; }
+template <bool Delta, int LL>
+constexpr auto seg_b_kernel() { return mvbk::vbyte_seg_decode<Delta, LL>; }
+
 template <bool Delta, int LL>
 int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cudaStream_t s, SegLaunch& sl) {
-    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
+    constexpr int kSmemB = seg_b_smem<LL>();
     static int per_sm = -1;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return MVB_ERR_CUDA;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return MVB_ERR_CUDA;
     if (per_sm < 0) {
-        if (cudaFuncSetAttribute(mvbk::vbyte_seg_decode<Delta, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(seg_b_kernel<Delta, LL>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_decode<Delta, LL>, mvbk::kSegThreads,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, seg_b_kernel<Delta, LL>(), seg_b_threads<LL>(),
                                                           kSmemB) != cudaSuccess)
             return MVB_ERR_CUDA;
         per_sm = n > 0 ? n : 1;
@@ -161,17 +169,24 @@ int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cu
         per_sm_a = n > 0 ? n : 1;
     }
     const long long ctas = static_cast<long long>(per_sm) * sms;
-    const long long warps = ctas * mvbk::kSegWarps;
+    const long long warps = ctas * (seg_b_threads<LL>() / 32);
     const long long qlen = p.mis + p.len;
     // segments per kernel-B warp: LL decodes a balanced contiguous run of them per
     // warp (finer is better balanced), V/EP hands them out round-robin
-    const long long per_warp = LL ? 8 : 4;
-    long long seg = (plan_len + per_warp * warps - 1) / (per_warp * warps);
-    seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: whole iterations
-    if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
+    // segments per kernel-B warp: LL decodes a static run and then pool segments
+    // (about 32 segments per warp: 1 KiB on c2), V/EP hands them out round-robin
+    long long seg;
+    {
+        const long long per_warp = LL ? 8 : 4;
+        seg = (plan_len + per_warp * warps - 1) / (per_warp * warps);
+        seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: whole iterations
+        if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
+    }
     const long long n_seg = (qlen + seg - 1) / seg;
     const long long n_grp = (n_seg + 31) / 32;
-    const size_t need = kHeaderBytes + 8 * static_cast<size_t>(n_seg) + 16 * static_cast<size_t>(n_grp);
+    const long long n_sup = (n_grp + 31) / 32;
+    const size_t need = kHeaderBytes + 8 * static_cast<size_t>(n_seg) + 16 * static_cast<size_t>(n_grp) +
+                        16 * static_cast<size_t>(n_sup);
     if (ws_bytes < need) return MVB_ERR_WORKSPACE;
     mvbk::SegParams& S = sl.S;
     S.in = p.in;
@@ -187,7 +202,10 @@ int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cu
     char* b = static_cast<char*>(ws) + kHeaderBytes;
     S.gcnt = reinterpret_cast<unsigned long long*>(b);
     S.gsum = S.gcnt + n_grp;
-    S.scnt = reinterpret_cast<unsigned*>(S.gsum + n_grp);
+    S.ucnt = S.gsum + n_grp;
+    S.usum = S.ucnt + n_sup;
+    S.n_sup = n_sup;
+    S.scnt = reinterpret_cast<unsigned*>(S.usum + n_sup);
     S.ssum = S.scnt + n_seg;
     S.hdr = p.hdr;
     S.res_dev = p.res_dev;
@@ -208,7 +226,7 @@ template <bool Delta, int LL>
 int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_launch,
                     volatile unsigned long long* chunk_total, const unsigned long long* base_in,
                     unsigned long long* base_out, cudaStream_t s) {
-    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
+    constexpr int kSmemB = seg_b_smem<LL>();
     mvbk::SegParams S = sl.S;
     S.s_lo = s_lo;
     S.s_hi = s_hi;
@@ -225,7 +243,7 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     // results in griddepcontrol.wait (hides B's launch latency behind A's tail)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid_b);
-    cfg.blockDim = dim3(mvbk::kSegThreads);
+    cfg.blockDim = dim3(seg_b_threads<LL>());
     cfg.dynamicSmemBytes = kSmemB;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -233,7 +251,7 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_seg_decode<Delta, LL>, S) != cudaSuccess) return MVB_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, seg_b_kernel<Delta, LL>(), S) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
@@ -585,7 +603,7 @@ int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint
     if (!c.init()) return MVB_ERR_CUDA;
     const size_t scan = scan_length(in_len, count);
     // the pipelined decode's segments can be finer than the one-shot decode's
-    const size_t wsb = std::max(mvb_workspace_bytes(scan), kHeaderBytes + 9 * (scan / 1024 + 2) + 64);
+    const size_t wsb = mvb_workspace_bytes(scan);
     if (!HostCtx::grow(c.d_in, c.in_cap, scan, false) || !HostCtx::grow(c.d_out, c.out_cap, count * 4, false) ||
         !HostCtx::grow(c.d_ws, c.ws_cap, wsb, true))
         return MVB_ERR_CUDA;
@@ -616,7 +634,10 @@ extern "C" {
 
 size_t mvb_workspace_bytes(size_t in_len) {
     const size_t a = ws_need(tiles_for(15, in_len) + 1), b = ws_need_warp(wtiles_for(15, in_len) + 1);
-    return a > b ? a : b;
+    // segmented decode with 1 KiB segments (the finest any launch uses)
+    const size_t n_seg = (in_len + 15) / 1024 + 1, n_grp = n_seg / 32 + 1, n_sup = n_grp / 32 + 1;
+    const size_t c = kHeaderBytes + 8 * n_seg + 16 * n_grp + 16 * n_sup;
+    return std::max(std::max(a, b), c);
 }
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
@@ -842,6 +863,13 @@ int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta
                        unsigned long long* trace) {
     return decode_device(in, in_len, count, delta != 0, prev, out, mode, res_dev, ws, ws_bytes, stream, trace);
 }
+
+#if MVB_TRACE_B
+// Internal profiling entry (trace builds only): kernel B's per-warp timeline buffer.
+int mvbx_set_trace_b(unsigned long long* buf) {
+    return cudaMemcpyToSymbol(mvbk::mvb_trace_b, &buf, sizeof(buf)) == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+#endif
 
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
