@@ -70,6 +70,7 @@ struct SegParams {
     unsigned long long* ucnt;  // per-supergroup (32 groups) sums of gcnt / gsum (zeroed likewise)
     unsigned long long* usum;
     long long n_sup;           // ceil(n_grp / 32)
+    long long a_it0, a_q, a_r; // kernel A: first iteration; iterations per warp (quotient, remainder)
     WsHeader* hdr;
     mvb_result* res_dev;
     // segments [s_lo, s_hi) of this launch pair (the whole stream, or one chunk
@@ -184,12 +185,15 @@ __global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const long long ns = S.s_hi - S.s_lo;
-    const long long s_begin = S.s_lo + gw * ns / nw, s_end = S.s_lo + (gw + 1) * ns / nw;  // balanced runs
+    // balanced runs of kSegASlice-byte iterations (host-computed quotient and
+    // remainder: no 64-bit division), independent of the segment boundaries
+    const long long it_begin = S.a_it0 + gw * S.a_q + (gw < S.a_r ? gw : S.a_r);
+    const long long it_end = it_begin + S.a_q + (gw < S.a_r ? 1 : 0);
     extern __shared__ __align__(128) uint8_t smem_a[];
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem_a)) +
                           static_cast<uint32_t>((threadIdx.x >> 5) * kAStages * kSegASlice);
-    if (s_begin < s_end) seg_totals_run<kDelta>(S, s_begin, s_end, lane, ring);
+    if (it_begin < it_end) seg_totals_run<kDelta>(S, it_begin, it_end, lane, ring);
+    (void)nw;
     // kernel B is launched as a programmatic dependent: it may start (and wait
     // in griddepcontrol.wait) once every CTA of this grid got here
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -231,11 +235,15 @@ __device__ __forceinline__ uint32_t words_digit_sum_hi(const uint32_t (&w)[kW]) 
 }
 
 template <bool kDelta>
-__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_begin, long long s_end, int lane,
+__device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_begin, long long it_end, int lane,
                                                uint32_t ring) {
+    // iterations it_begin .. it_end - 1 of kSegASlice bytes (q = kSegASlice * it);
+    // a segment is its_per_seg iterations.  The run's totals go to the segment,
+    // group and supergroup accumulators (atomics; zero between launches) each
+    // time the run leaves a segment.
     const int its_per_seg = static_cast<int>(S.seg_bytes / kSegASlice);
-    const long long q_begin = s_begin * S.seg_bytes, q_end = s_end * S.seg_bytes;
-    const int n_it = static_cast<int>((q_end - q_begin) / kSegASlice);
+    const long long q_begin = it_begin * kSegASlice;
+    const int n_it = static_cast<int>(it_end - it_begin);
     int i_lo, i_hi;  // iterations whose kSegASlice bytes all lie inside the stream: i_lo <= it < i_hi
     {
         const long long d = S.mis - q_begin, e = S.mis + S.len - q_begin;
@@ -269,12 +277,11 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         }
         cp_async_commit();
     }
-    unsigned cnt = 0;
+    uint32_t ccont = 0;  // 128 x continuation bytes of the lane in the current segment (dp4a)
     uint32_t sum = 0;
-    unsigned long long gc = 0, gs = 0;  // totals of the run's segments in the current group
-    unsigned long long uc = 0, us = 0;  // ... in the current supergroup
-    long long s = s_begin;
-    int it_s = 0;  // iteration within segment s
+    long long s = it_begin / its_per_seg;
+    int it_s = static_cast<int>(it_begin - s * its_per_seg);  // iteration within segment s
+    uint32_t nbytes = 0;                                      // bytes of the run inside segment s
     for (int it = 0; it < n_it; ++it) {
         {
             const int jn = it + kAStages - 1;
@@ -311,59 +318,43 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
         }
         pw2 = l2;
         pw3 = l3;
-        const bool seg_last = it_s == its_per_seg - 1;
         if (inter) {
-            unsigned nc = 0;
 #pragma unroll
-            for (int k = 2; k < kSegAW; ++k) nc += __popc(w[k] & 0x80808080u);
-            cnt += L - nc;
-        } else {
+            for (int k = 2; k < kSegAW; ++k) ccont = __dp4a(w[k] & 0x80808080u, 0x01010101u, ccont);
+            nbytes += L;
+        } else {  // terminators in the stream only: count them directly
             const long long ql = q_begin + static_cast<long long>(kSegASlice) * it + L * lane;
+            uint32_t t = 0;
 #pragma unroll
             for (int c = 0; c < kSegAChunks; ++c) {
                 const uint32_t T16 = hibits16(~w[2 + 4 * c], ~w[3 + 4 * c], ~w[4 + 4 * c], ~w[5 + 4 * c]);
-                cnt += __popc(T16 & seg_inr16(S, ql + 16 * c));
+                t += __popc(T16 & seg_inr16(S, ql + 16 * c));
             }
+            nbytes += t;  // (bytes - continuation bytes = terminators: count them as "bytes")
         }
         if (kDelta) {
             uint32_t hi = 0;
             sum += words_digit_sum(w, hi);
             if (__any_sync(0xFFFFFFFFu, hi)) sum += words_digit_sum_hi(w);  // integers of 3..5 bytes
         }
-        if (seg_last) {
-            const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
+        if (++it_s == its_per_seg || it + 1 == n_it) {  // leaving segment s: flush
+            const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, nbytes - (ccont >> 7));
             const uint32_t s_tot = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sum) : 0u;
             if (lane == 0) {
-                S.scnt[s] = c_tot;
-                if (kDelta) S.ssum[s] = s_tot;
-            }
-            // group accumulators: one atomic per group the run touches
-            gc += c_tot;
-            gs += s_tot;
-            if (((s + 1) & 31) == 0 || s + 1 == s_end) {
-                if (lane == 0) {
-                    atomicAdd(S.gcnt + (s >> 5), gc);
-                    if (kDelta) atomicAdd(S.gsum + (s >> 5), gs);
-                }
-                uc += gc;
-                us += gs;
-                gc = 0;
-                gs = 0;
-                if (((s + 1) & 1023) == 0 || s + 1 == s_end) {  // supergroup accumulators (32 groups)
-                    if (lane == 0) {
-                        atomicAdd(S.ucnt + (s >> 10), uc);
-                        if (kDelta) atomicAdd(S.usum + (s >> 10), us);
-                    }
-                    uc = 0;
-                    us = 0;
+                atomicAdd(S.scnt + s, c_tot);
+                atomicAdd(reinterpret_cast<unsigned long long*>(S.gcnt + (s >> 5)), static_cast<unsigned long long>(c_tot));
+                atomicAdd(S.ucnt + (s >> 10), static_cast<unsigned long long>(c_tot));
+                if (kDelta) {
+                    atomicAdd(S.ssum + s, s_tot);
+                    atomicAdd(S.gsum + (s >> 5), static_cast<unsigned long long>(s_tot));
+                    atomicAdd(S.usum + (s >> 10), static_cast<unsigned long long>(s_tot));
                 }
             }
-            cnt = 0;
+            ccont = 0;
             sum = 0;
+            nbytes = 0;
             ++s;
             it_s = 0;
-        } else {
-            ++it_s;
         }
     }
 }
@@ -1373,7 +1364,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     }
     // the end of the range's last integer: in slice last_i
     long long last_end = -1;
-    if (last_i >= 0) {
+    if (last_i >= 0 && !K.hdr) {  // (a stream decode finds the stream's last integer in its completion)
         const long long q0 = qs + static_cast<long long>(kLLSlice) * last_i + 32 * lane;
         const uint4 x0 = r_load16(R, q0), x1 = r_load16(R, q0 + 16);
         const uint32_t e0 = hibits16(~x0.x, ~x0.y, ~x0.z, ~x0.w) & r_inr16(R, q0);
@@ -1493,7 +1484,7 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
     }
     // the end of the range's last integer: in slice last_i
     long long last_end = -1;
-    if (last_i >= 0) {
+    if (last_i >= 0 && !K.hdr) {  // (a stream decode finds the stream's last integer in its completion)
         const long long q0 = qs + static_cast<long long>(kSegSlice) * last_i + 16 * lane;
         const uint4 x = r_load16(R, q0);
         const uint32_t e16 = hibits16(~x.x, ~x.y, ~x.z, ~x.w) & r_inr16(R, q0);
@@ -1610,6 +1601,13 @@ __device__ __forceinline__ void seg_complete(const SegParams& S, bool find_last_
                 le = x > le ? x : le;
             }
             last_end_found = le > 0 ? le : 0;
+        }
+    }
+    if (!S.base_in) {  // whole-stream launch: zero the segment totals (a pipelined decode's host memsets them)
+        __syncthreads();
+        for (long long k = S.s_lo + threadIdx.x; k < S.s_hi; k += blockDim.x) {
+            S.scnt[k] = 0;
+            S.ssum[k] = 0;
         }
     }
     if (threadIdx.x == 0) {
@@ -1758,7 +1756,8 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
         else
             decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
                                  lane, K, ro);
-        if (lane == 0 && ro.last_end >= 0) atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
+        if (!kLL && lane == 0 && ro.last_end >= 0)
+            atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
     }
 #if MVB_TRACE_B
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[3]));
@@ -1776,7 +1775,7 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
 #endif
 
     // ---- completion; the last CTA produces the DecodeResult ----
-    seg_complete<kSegWarps>(S, false);
+    seg_complete<kSegWarps>(S, kLL != 0);
 }
 
 // ------------------------------------------------------------------ batched lists

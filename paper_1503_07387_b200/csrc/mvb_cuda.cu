@@ -22,6 +22,10 @@
 #include "totals_kernel.cuh"
 #include "encode_kernel.cuh"
 
+#ifndef MVB_A_ITS
+#define MVB_A_ITS 8  // kernel A: at least this many 1 KiB iterations per warp
+#endif
+
 namespace {
 
 using mvbk::Params;
@@ -128,7 +132,7 @@ cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
 // segments [s_lo, s_hi).
 struct SegLaunch {
     mvbk::SegParams S;
-    unsigned grid_a_cap, grid_b_cap;
+    unsigned grid_a_cap, grid_b_cap, grid_a_launch;
 };
 
 // LL: 0 V/EP range decode (choice 5), 1 lane-local (choice 0, default).
@@ -177,7 +181,7 @@ int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cu
     // (about 32 segments per warp: 1 KiB on c2), V/EP hands them out round-robin
     long long seg;
     {
-        const long long per_warp = LL ? 8 : 4;
+        const long long per_warp = LL ? 1 : 4;  // LL: one segment (a balanced byte range) per warp
         seg = (plan_len + per_warp * warps - 1) / (per_warp * warps);
         seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: whole iterations
         if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
@@ -236,7 +240,27 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     S.base_out = base_out;
     const long long n = s_hi - s_lo;
     const long long ga = (n + mvbk::kSegWarps - 1) / mvbk::kSegWarps;  // at least one segment per warp
-    const unsigned grid_a = static_cast<unsigned>(ga < sl.grid_a_cap ? ga : sl.grid_a_cap);
+    // kernel A: balanced runs of at least MVB_A_ITS iterations per warp over the
+    // launch's segments (clipped to the stream)
+    {
+        const long long its_per_seg = S.seg_bytes / mvbk::kSegASlice;
+        const long long qlen = S.mis + S.len;
+        const long long it0 = s_lo * its_per_seg;
+        long long it1 = s_hi * its_per_seg;
+        const long long it_stream = (qlen + mvbk::kSegASlice - 1) / mvbk::kSegASlice;
+        if (it1 > it_stream) it1 = it_stream;
+        const long long n_it = it1 > it0 ? it1 - it0 : 0;
+        long long wa = (n_it + MVB_A_ITS - 1) / MVB_A_ITS;
+        const long long wa_cap = static_cast<long long>(sl.grid_a_cap) * mvbk::kSegWarps;
+        if (wa > wa_cap) wa = wa_cap;
+        if (wa < 1) wa = 1;
+        wa = (wa + mvbk::kSegWarps - 1) / mvbk::kSegWarps * mvbk::kSegWarps;
+        S.a_it0 = it0;
+        S.a_q = n_it / wa;
+        S.a_r = n_it % wa;
+        sl.grid_a_launch = static_cast<unsigned>(wa / mvbk::kSegWarps);
+    }
+    const unsigned grid_a = sl.grid_a_launch;
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
     const unsigned grid_b = static_cast<unsigned>(ga < sl.grid_b_cap ? ga : sl.grid_b_cap);
     // programmatic dependent launch: B's CTAs launch as A's retire and wait for A's
@@ -563,6 +587,11 @@ int decode_host_pipelined(HostCtx& c, const uint8_t* in, size_t scan, size_t cou
         const int e = seg_launch_pair<Delta, 1>(sl, cb[k], cb[k + 1], k == n_chunks - 1, c.dm_tot + k,
                                                 k ? c.d_base + 2 * k : nullptr, c.d_base + 2 * (k + 1), c.stream);
         if (e) return e;
+        if (k == n_chunks - 1 && k > 0) {  // segment totals are zero between decodes
+            if (cudaMemsetAsync(sl.S.scnt, 0, 4 * static_cast<size_t>(n_seg), c.stream) != cudaSuccess ||
+                cudaMemsetAsync(sl.S.ssum, 0, 4 * static_cast<size_t>(n_seg), c.stream) != cudaSuccess)
+                return MVB_ERR_CUDA;
+        }
         return cudaEventRecord(c.ev_dec[k], c.stream) == cudaSuccess ? 0 : MVB_ERR_CUDA;
     };
     if (cudaEventRecord(c.ev_start, c.h2d) != cudaSuccess) return MVB_ERR_CUDA;
