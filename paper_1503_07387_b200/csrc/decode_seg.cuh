@@ -277,38 +277,49 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
         }
         cp_async_commit();
     }
-    uint32_t ccont = 0;  // 128 x continuation bytes of the lane in the current segment (dp4a)
-    uint32_t sum = 0;
+    uint32_t tcount = 0;  // terminators of the lane's bytes (inside the stream) in the current segment
+    uint32_t sum = 0;     // digit-weight sum of the lane's bytes in the current segment
     long long s = it_begin / its_per_seg;
-    int it_s = static_cast<int>(it_begin - s * its_per_seg);  // iteration within segment s
-    uint32_t nbytes = 0;                                      // bytes of the run inside segment s
+    int to_flush = its_per_seg - static_cast<int>(it_begin - s * its_per_seg);  // iterations left in segment s
+    const uint8_t* pf = pin + static_cast<long long>(kSegASlice) * (kAStages - 1);  // prefetch source of it + 3
+    uint32_t rd = 0;                                                             // ring offset of iteration it
     for (int it = 0; it < n_it; ++it) {
         {
             const int jn = it + kAStages - 1;
-            if (jn < n_it && jn >= i_lo && jn < i_hi) {
-                const uint32_t d = rb + kSegASlice * (jn & (kAStages - 1));
+            if (jn >= i_lo && jn < i_hi) {
+                const uint32_t d = rb + ((rd + kSegASlice * (kAStages - 1)) & (kSegASlice * kAStages - 1));
 #pragma unroll
-                for (int c = 0; c < kSegAChunks; ++c)
-                    cp_async16(d + 16 * c, pin + static_cast<long long>(kSegASlice) * jn + 16 * c);
+                for (int c = 0; c < kSegAChunks; ++c) cp_async16(d + 16 * c, pf + 16 * c);
             }
             cp_async_commit();
+            pf += kSegASlice;
         }
-        const bool inter = it >= i_lo && it < i_hi;
+        const bool inter = it >= i_lo && it < i_hi;  // (warp-uniform)
         uint32_t w[kSegAW];  // w[0], w[1]: the 8 bytes before this lane's bytes; then the lane's words
+        uint32_t term = 0;   // edge iterations: terminators inside the stream
+        if (inter) {
+            cp_async_wait<kAStages - 1>();
 #pragma unroll
-        for (int c = 0; c < kSegAChunks; ++c) {
-            uint4 x;
-            if (inter) {
-                if (c == 0) cp_async_wait<kAStages - 1>();
-                x = lds128(rb + kSegASlice * (it & (kAStages - 1)) + 16 * c);
-            } else {
-                x = seg_load16(S, q_begin + static_cast<long long>(kSegASlice) * it + L * lane + 16 * c);
+            for (int c = 0; c < kSegAChunks; ++c) {
+                const uint4 x = lds128(rb + rd + 16 * c);
+                w[2 + 4 * c] = x.x;
+                w[3 + 4 * c] = x.y;
+                w[4 + 4 * c] = x.z;
+                w[5 + 4 * c] = x.w;
             }
-            w[2 + 4 * c] = x.x;
-            w[3 + 4 * c] = x.y;
-            w[4 + 4 * c] = x.z;
-            w[5 + 4 * c] = x.w;
+        } else {
+            const long long ql = q_begin + static_cast<long long>(kSegASlice) * it + L * lane;
+#pragma unroll
+            for (int c = 0; c < kSegAChunks; ++c) {
+                const uint4 x = seg_load16(S, ql + 16 * c);
+                w[2 + 4 * c] = x.x;
+                w[3 + 4 * c] = x.y;
+                w[4 + 4 * c] = x.z;
+                w[5 + 4 * c] = x.w;
+                term += __popc(hibits16(~x.x, ~x.y, ~x.z, ~x.w) & seg_inr16(S, ql + 16 * c));
+            }
         }
+        rd = (rd + kSegASlice) & (kSegASlice * kAStages - 1);
         w[0] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 2], 1);
         w[1] = __shfl_up_sync(0xFFFFFFFFu, w[kSegAW - 1], 1);
         const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w[kSegAW - 2], 31), l3 = __shfl_sync(0xFFFFFFFFu, w[kSegAW - 1], 31);
@@ -318,31 +329,40 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
         }
         pw2 = l2;
         pw3 = l3;
-        if (inter) {
+        // per word, split between the ALU and FMA pipes: ck = continuation bits,
+        // c1b = bit 0 of byte j set if byte j-1 continues, weight 1 or 128 per
+        // byte (IMAD); the digit-weight sum is dp4a(w, wt) - dp4a(ck, wt) (the
+        // high bits weighed in and out again, no 0x7F mask); the continuation
+        // bytes accumulate in byte counters
+        uint32_t cb = 0, sa = 0, sb = 0;
+        uint32_t cp = w[1] & 0x80808080u;
 #pragma unroll
-            for (int k = 2; k < kSegAW; ++k) ccont = __dp4a(w[k] & 0x80808080u, 0x01010101u, ccont);
-            nbytes += L;
-        } else {  // terminators in the stream only: count them directly
-            const long long ql = q_begin + static_cast<long long>(kSegASlice) * it + L * lane;
-            uint32_t t = 0;
-#pragma unroll
-            for (int c = 0; c < kSegAChunks; ++c) {
-                const uint32_t T16 = hibits16(~w[2 + 4 * c], ~w[3 + 4 * c], ~w[4 + 4 * c], ~w[5 + 4 * c]);
-                t += __popc(T16 & seg_inr16(S, ql + 16 * c));
-            }
-            nbytes += t;  // (bytes - continuation bytes = terminators: count them as "bytes")
+        for (int k = 2; k < kSegAW; ++k) {
+            const uint32_t ck = w[k] & 0x80808080u;
+            const uint32_t c1b = __funnelshift_l(cp, ck, 1);
+            const uint32_t wt = c1b * 127u + 0x01010101u;
+            sa = __dp4a(w[k], wt, sa);
+            sb = __dp4a(ck, wt, sb);
+            cb += ck >> 7;
+            cp = ck;
         }
+        const uint32_t nc = __dp4a(cb, 0x01010101u, 0u);  // continuation bytes of the lane's L bytes
+        tcount += inter ? static_cast<uint32_t>(L) - nc : term;
         if (kDelta) {
-            uint32_t hi = 0;
-            sum += words_digit_sum(w, hi);
-            if (__any_sync(0xFFFFFFFFu, hi)) sum += words_digit_sum_hi(w);  // integers of 3..5 bytes
+            sum += sa - sb;
+            // sb = 128 x (the weights of the continuation bytes) = 128 x nc unless a
+            // continuation byte follows another (bytes 0..31, or bytes -2, -1 in
+            // the halo): an integer of 3..5 bytes, whose later bytes need the
+            // weights 2^14 / 2^21 / 2^28
+            const bool pair = sb != (nc << 7) || ((w[1] & (w[1] << 8)) >> 31);
+            if (__any_sync(0xFFFFFFFFu, pair)) sum += words_digit_sum_hi(w);
         }
-        if (++it_s == its_per_seg || it + 1 == n_it) {  // leaving segment s: flush
-            const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, nbytes - (ccont >> 7));
+        if (--to_flush == 0 || it + 1 == n_it) {  // leaving segment s: flush
+            const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, tcount);
             const uint32_t s_tot = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sum) : 0u;
             if (lane == 0) {
                 atomicAdd(S.scnt + s, c_tot);
-                atomicAdd(reinterpret_cast<unsigned long long*>(S.gcnt + (s >> 5)), static_cast<unsigned long long>(c_tot));
+                atomicAdd(S.gcnt + (s >> 5), static_cast<unsigned long long>(c_tot));
                 atomicAdd(S.ucnt + (s >> 10), static_cast<unsigned long long>(c_tot));
                 if (kDelta) {
                     atomicAdd(S.ssum + s, s_tot);
@@ -350,11 +370,10 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
                     atomicAdd(S.usum + (s >> 10), static_cast<unsigned long long>(s_tot));
                 }
             }
-            ccont = 0;
+            tcount = 0;
             sum = 0;
-            nbytes = 0;
             ++s;
-            it_s = 0;
+            to_flush = its_per_seg;
         }
     }
 }
@@ -809,6 +828,47 @@ __device__ __forceinline__ void lane_slots_fast16(uint32_t wp3, uint32_t w0, uin
 // Delta: the lane's integer sum is two dp4a per word over the terminator
 // bytes (its integers are complete: an integer straddling into the lane is
 // built from the previous lane's last byte), then the warp scan.
+// PTX of the 1-2-byte slots (operands: %0 staging pointer, %1 running sum,
+// %2 terminator mask, then the A words, then the B words).  One slot: the
+// candidate (prmt), the terminator predicate, (the running sum,) the store,
+// the pointer bump; S1 swizzles the staging address (see stg_addr).
+#define MVB_S2_SLOT_D0S0(A, B, SEL, M) \
+    "prmt.b32 v, " A ", " B ", " SEL ";\n\tand.b32 t, %2, " M ";\n\tsetp.ne.b32 p, t, 0;\n\t" \
+    "@p st.shared.u32 [%0], v;\n\t@p add.u32 %0, %0, 4;\n\t"
+#define MVB_S2_SLOT_D1S0(A, B, SEL, M) \
+    "prmt.b32 v, " A ", " B ", " SEL ";\n\tand.b32 t, %2, " M ";\n\tsetp.ne.b32 p, t, 0;\n\t" \
+    "@p add.u32 %1, %1, v;\n\t@p st.shared.u32 [%0], %1;\n\t@p add.u32 %0, %0, 4;\n\t"
+#define MVB_S2_SLOT_D0S1(A, B, SEL, M) \
+    "prmt.b32 v, " A ", " B ", " SEL ";\n\tand.b32 t, %2, " M ";\n\tsetp.ne.b32 p, t, 0;\n\t" \
+    "shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t" \
+    "@p st.shared.u32 [t], v;\n\t@p add.u32 %0, %0, 4;\n\t"
+#define MVB_S2_SLOT_D1S1(A, B, SEL, M) \
+    "prmt.b32 v, " A ", " B ", " SEL ";\n\tand.b32 t, %2, " M ";\n\tsetp.ne.b32 p, t, 0;\n\t" \
+    "@p add.u32 %1, %1, v;\n\tshr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t" \
+    "@p st.shared.u32 [t], %1;\n\t@p add.u32 %0, %0, 4;\n\t"
+#define MVB_S2_WORD(SLOT, A, B, M0, M1, M2, M3) \
+    SLOT(A, B, "0xcc40", M0) SLOT(A, B, "0xdd51", M1) SLOT(A, B, "0xee62", M2) SLOT(A, B, "0xff73", M3)
+#define MVB_S2_BLOCK4(SLOT)                                                                         \
+    "{\n\t.reg .pred p;\n\t.reg .b32 v, t;\n\t"                                                    \
+    MVB_S2_WORD(SLOT, "%3", "%7", "0x1", "0x2", "0x4", "0x8")                                       \
+    MVB_S2_WORD(SLOT, "%4", "%8", "0x10", "0x20", "0x40", "0x80")                                   \
+    MVB_S2_WORD(SLOT, "%5", "%9", "0x100", "0x200", "0x400", "0x800")                               \
+    MVB_S2_WORD(SLOT, "%6", "%10", "0x1000", "0x2000", "0x4000", "0x8000") "}"
+#define MVB_S2_BLOCK8(SLOT)                                                                         \
+    "{\n\t.reg .pred p;\n\t.reg .b32 v, t;\n\t"                                                    \
+    MVB_S2_WORD(SLOT, "%3", "%11", "0x1", "0x2", "0x4", "0x8")                                      \
+    MVB_S2_WORD(SLOT, "%4", "%12", "0x10", "0x20", "0x40", "0x80")                                  \
+    MVB_S2_WORD(SLOT, "%5", "%13", "0x100", "0x200", "0x400", "0x800")                              \
+    MVB_S2_WORD(SLOT, "%6", "%14", "0x1000", "0x2000", "0x4000", "0x8000")                          \
+    MVB_S2_WORD(SLOT, "%7", "%15", "0x10000", "0x20000", "0x40000", "0x80000")                      \
+    MVB_S2_WORD(SLOT, "%8", "%16", "0x100000", "0x200000", "0x400000", "0x800000")                  \
+    MVB_S2_WORD(SLOT, "%9", "%17", "0x1000000", "0x2000000", "0x4000000", "0x8000000")              \
+    MVB_S2_WORD(SLOT, "%10", "%18", "0x10000000", "0x20000000", "0x40000000", "0x80000000") "}"
+#define MVB_S2_OPS4 "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(B[0]), "r"(B[1]), "r"(B[2]), "r"(B[3])
+#define MVB_S2_OPS8                                                                                 \
+    "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(A[4]), "r"(A[5]), "r"(A[6]), "r"(A[7]), "r"(B[0]), \
+        "r"(B[1]), "r"(B[2]), "r"(B[3]), "r"(B[4]), "r"(B[5]), "r"(B[6]), "r"(B[7])
+
 __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -835,44 +895,24 @@ __device__ __forceinline__ void lane_slots_2b(uint32_t wp3, const uint32_t (&w)[
     }
     uint32_t acc = 0;
     if (kDelta) acc = lane_scan_offset<kDelta>(own, carry);
-#pragma unroll
-    for (int e = 0; e < 4 * NW; ++e) {
-        const int k = e >> 2, t = e & 3;
-        const uint32_t sel = static_cast<uint32_t>(t | ((4 + t) << 4) | ((12 + t) << 8) | ((12 + t) << 12));
-        const uint32_t v = prmt_sign(A[k], B[k], sel);
-        if (kDelta) {
-#define MVB_SLOT2_DELTA(STORE)                                                         \
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
-                 "and.b32 t, %2, %4;\n\t"                                                \
-                 "setp.ne.b32 p, t, 0;\n\t"                                              \
-                 "@p add.u32 %1, %1, %3;\n\t" STORE                                      \
-                 "@p add.u32 %0, %0, 4;\n\t"                                             \
-                 "}"                                                                        \
-                 : "+r"(sp), "+r"(acc)                                                      \
-                 : "r"(T), "r"(v), "r"(1u << e)                                             \
-                 : "memory")
-            if (kSwz)
-                MVB_SLOT2_DELTA("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
-                                "@p st.shared.u32 [t], %1;\n\t");
-            else
-                MVB_SLOT2_DELTA("@p st.shared.u32 [%0], %1;\n\t");
-#undef MVB_SLOT2_DELTA
+    // all 4 * NW slots in one asm block: straight-line predicated code with
+    // the pointer and the running sum in fixed registers (separate asm
+    // statements per slot made ptxas copy them between slots)
+    if constexpr (NW == 4) {
+        if (kSwz) {
+            if (kDelta) asm volatile(MVB_S2_BLOCK4(MVB_S2_SLOT_D1S1) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS4 : "memory");
+            else asm volatile(MVB_S2_BLOCK4(MVB_S2_SLOT_D0S1) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS4 : "memory");
         } else {
-#define MVB_SLOT2_PLAIN(STORE)                                                         \
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"                              \
-                 "and.b32 t, %1, %3;\n\t"                                                \
-                 "setp.ne.b32 p, t, 0;\n\t" STORE                                        \
-                 "@p add.u32 %0, %0, 4;\n\t"                                             \
-                 "}"                                                                        \
-                 : "+r"(sp)                                                                 \
-                 : "r"(T), "r"(v), "r"(1u << e)                                             \
-                 : "memory")
-            if (kSwz)
-                MVB_SLOT2_PLAIN("shr.b32 t, %0, 3;\n\tand.b32 t, t, 0x70;\n\txor.b32 t, t, %0;\n\t"
-                                "@p st.shared.u32 [t], %2;\n\t");
-            else
-                MVB_SLOT2_PLAIN("@p st.shared.u32 [%0], %2;\n\t");
-#undef MVB_SLOT2_PLAIN
+            if (kDelta) asm volatile(MVB_S2_BLOCK4(MVB_S2_SLOT_D1S0) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS4 : "memory");
+            else asm volatile(MVB_S2_BLOCK4(MVB_S2_SLOT_D0S0) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS4 : "memory");
+        }
+    } else {
+        if (kSwz) {
+            if (kDelta) asm volatile(MVB_S2_BLOCK8(MVB_S2_SLOT_D1S1) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS8 : "memory");
+            else asm volatile(MVB_S2_BLOCK8(MVB_S2_SLOT_D0S1) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS8 : "memory");
+        } else {
+            if (kDelta) asm volatile(MVB_S2_BLOCK8(MVB_S2_SLOT_D1S0) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS8 : "memory");
+            else asm volatile(MVB_S2_BLOCK8(MVB_S2_SLOT_D0S0) : "+r"(sp), "+r"(acc) : "r"(T), MVB_S2_OPS8 : "memory");
         }
     }
 }
@@ -918,11 +958,11 @@ __device__ __forceinline__ void lane_slots_gen16(uint32_t wp3, uint32_t w0, uint
 // The general path of one slice (after the count scan): malformed integers,
 // the end of integer limit-1, then the general slots.
 template <bool kDelta, bool kSwz>
-__device__ __noinline__ void ll_slice_gen16(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
+__device__ __noinline__ uint32_t ll_slice_gen16(const ByteRange& R, long long q0, uint32_t w0, uint32_t w1, uint32_t w2,
                                           uint32_t w3, uint32_t wp3, uint32_t T16, uint32_t inr16, uint32_t n_own,
                                           uint32_t n_w, uint32_t wexcl, unsigned long long rs,
                                           unsigned long long limit, const RangeSink& K, uint32_t sp,
-                                          uint32_t& carry) {
+                                          uint32_t carry) {
     const int lane = threadIdx.x & 31;
     const uint32_t ends16 = T16 & inr16;
     uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1);
@@ -957,7 +997,7 @@ __device__ __noinline__ void ll_slice_gen16(const ByteRange& R, long long q0, ui
         }
         if (lane == 0) sink_error(K, idx, pos, limit);
     }
-    if (n_w == 0) return;
+    if (n_w == 0) return carry;
     // end of integer limit-1, if it ends in this slice
     if (limit - rs <= n_w && limit - 1 - rs >= wexcl && limit - 1 - rs < wexcl + n_own) {
         uint32_t m = ends16;
@@ -965,6 +1005,7 @@ __device__ __noinline__ void ll_slice_gen16(const ByteRange& R, long long q0, ui
         sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
     }
     lane_slots_gen16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, ends16, sp, carry);
+    return carry;  // (by value: a noinline function's reference argument lives on the stack)
 }
 
 // ---- 32-byte lanes (plain decodes): 1 KiB slices ----
@@ -1192,16 +1233,16 @@ __device__ __forceinline__ void gen_sparse_plain(uint32_t wp3, const uint4 x0, c
 // halves): strict checks, then the general slots.  Delta: both halves' sums
 // first (the output order is lane-major), one warp scan, then the stores.
 template <bool kDelta, bool kSwz>
-__device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
+__device__ __noinline__ uint32_t ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
                                           uint32_t wp2, uint32_t wp3, uint32_t T32, uint32_t inr32, uint32_t n_w,
                                           uint32_t wexcl, unsigned long long rs, unsigned long long limit,
-                                          const RangeSink& K, uint32_t sp, uint32_t win, uint32_t& carry) {
+                                          const RangeSink& K, uint32_t sp, uint32_t win, uint32_t carry) {
     const uint32_t e0 = T32 & inr32 & 0xFFFFu, e1 = (T32 & inr32) >> 16;
     gen_check_half(R, q0, x0.x, x0.y, x0.z, x0.w, wp2, wp3, T32 & 0xFFFFu, inr32 & 0xFFFFu, n_w, wexcl, rs, limit,
                    K);
     gen_check_half(R, q0 + 16, x1.x, x1.y, x1.z, x1.w, x0.z, x0.w, T32 >> 16, inr32 >> 16, n_w,
                    wexcl + __popc(e0), rs, limit, K);
-    if (n_w == 0) return;
+    if (n_w == 0) return carry;
     const uint32_t sp1 = sp + 4u * __popc(e0);
     if (kDelta) {
         const uint32_t s0 = gen_half<0, kSwz>(wp3, x0.x, x0.y, x0.z, x0.w, T32 & 0xFFFFu, e0, 0u, 0u);
@@ -1218,6 +1259,7 @@ __device__ __noinline__ void ll_slice_gen(const ByteRange& R, long long q0, cons
             gen_half<1, kSwz>(x0.w, x1.x, x1.y, x1.z, x1.w, T32 >> 16, e1, sp1, 0u);
         }
     }
+    return carry;
 }
 
 // Copy stage[a, a + n) to out[run, run + n), indices below `limit` only;
@@ -1353,8 +1395,8 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         else if (ok_range && !(vote & 2u))
             lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
         else
-            ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
-                                       st_base + 4u * (a + wexcl), ring + 2u * kLLSlice + 72u * lane, carry);
+            carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
+                                               st_base + 4u * (a + wexcl), ring + 2u * kLLSlice + 72u * lane, carry);
         left = left > n_w ? left - n_w : 0u;
         if (n_w == 0) continue;
         __syncwarp();
@@ -1470,9 +1512,9 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             } else if (ok_range && !(vote & 2u))
                 lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
             else
-                ll_slice_gen16<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0, w1, w2, w3,
-                                           wp3, T16, inr16, n_own, n_w, wexcl, run + n_g, limit, K,
-                                           st_base + 4u * (a + n_g + wexcl), carry);
+                carry = ll_slice_gen16<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0,
+                                                     w1, w2, w3, wp3, T16, inr16, n_own, n_w, wexcl, run + n_g, limit,
+                                                     K, st_base + 4u * (a + n_g + wexcl), carry);
             n_g += n_w;
             left = left > n_w ? left - n_w : 0u;
         }
