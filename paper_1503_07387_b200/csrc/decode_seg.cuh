@@ -663,7 +663,7 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 // registers, the warp scan of the lane totals adds the offsets before the
 // stores.
 #ifndef MVB_DELTA32
-#define MVB_DELTA32 0  // 1: delta decodes on 32-byte lanes too (fewer instructions, longer dependency chains: slower on c2)
+#define MVB_DELTA32 1  // delta stream decodes on 32-byte lanes too (0: 16-byte lanes, two slices per staging group)
 #endif
 #ifndef MVB_LL_BLOCKS
 #define MVB_LL_BLOCKS 6
@@ -1541,16 +1541,19 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
     ro.n = run - base;
 }
 
-// The lane-local range decode: 16-byte lanes for delta decodes (their SWAR
-// prefix and running sums keep within the 80-register budget), 32-byte lanes
-// for plain decodes (half the per-slice fixed work per byte).
+// The lane-local range decode: 32-byte lanes (half the per-slice fixed work
+// per byte of 16-byte lanes); batched delta lists keep 16-byte lanes.
 template <bool kDelta, bool kSwz>
 __device__ __forceinline__ void decode_range_llw(const ByteRange& R, long long qs, long long qe,
                                                  unsigned long long base, uint32_t carry, unsigned long long limit,
                                                  uint32_t* out, uint32_t* stage, uint32_t ring, int lane,
                                                  const RangeSink& K, RangeOut& ro) {
-    if (kDelta && !MVB_DELTA32) decode_range_ll16<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
-    else decode_range_ll<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
+    // (batched lists -- K.hdr null -- keep 16-byte lanes for delta: most lists are
+    // short, and 1 KiB slices would mostly be padding)
+    if (kDelta && (!MVB_DELTA32 || !K.hdr))
+        decode_range_ll16<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
+    else
+        decode_range_ll<kDelta, kSwz>(R, qs, qe, base, carry, limit, out, stage, ring, lane, K, ro);
 }
 
 // Completion of a kernel-B launch (all threads of every CTA call it): the
@@ -1788,11 +1791,15 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
             unsigned long long rc = (s + lane < s_end) ? S.scnt[s + lane] : 0u;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
-            if (range_dense(rc, (s_end - s) * S.seg_bytes))
-                decode_range_llw<kDelta, true>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+            // the last segment ends with the stream (no slices of padding: they hold no
+            // integer and would all take the masked general path)
+            const long long q_stream_end = (R.hi + 15) & ~15ll;
+            const long long qe = s_end * S.seg_bytes < q_stream_end ? s_end * S.seg_bytes : q_stream_end;
+            if (range_dense(rc, qe - s * S.seg_bytes))
+                decode_range_llw<kDelta, true>(R, s * S.seg_bytes, qe, base, carry, S.count, S.out,
                                               reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
             else
-                decode_range_llw<kDelta, false>(R, s * S.seg_bytes, s_end * S.seg_bytes, base, carry, S.count, S.out,
+                decode_range_llw<kDelta, false>(R, s * S.seg_bytes, qe, base, carry, S.count, S.out,
                                                reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
         }
         else

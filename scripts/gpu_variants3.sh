@@ -9,7 +9,8 @@ from paper_1503_07387_b200 import _lib, mvb, workload as W
 dev = torch.device("cuda", 0)
 choices = [int(c) for c in os.environ["CHOICES"].split()]
 mk = {"c2": W.config2, "c1": W.config1, "all1": lambda: W.config5("all1"), "all5": lambda: W.config5("all5"),
-      "p50": lambda: W.config5("p50"), "p50d": lambda: W.config5("p50", delta=True)}
+      "p50": lambda: W.config5("p50"), "p50d": lambda: W.config5("p50", delta=True),
+      "c4s": lambda: W.config4(n=1 << 27)}
 for name in os.environ["CFGS"].split():
     w = mk[name]()
     per = w.encoded.size + 4 * w.count

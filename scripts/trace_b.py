@@ -51,3 +51,5 @@ print("  ends  ", np.round(en[sel], 2).tolist())
 k2 = min(ends, key=lambda x: ends[x][1])
 sel2 = np.where(sm == k2)[0]
 print(f"fastest SM {k2}: warps {sel2[:24].tolist()}")
+order = np.argsort(-en)[:6]
+print("latest warps:", [(int(i), round(float(en[i]), 2), round(float(pf[i] - wt[i]), 2), int(sm[i])) for i in order])
