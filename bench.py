@@ -290,7 +290,9 @@ def run_ours(args):
             i += 1
         torch.cuda.synchronize()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # the timed region holds only the decodes: events between them would cost ~5 us
+    # each (they break the back-to-back launch of kernel A behind the previous
+    # kernel B), so a decode's duration is the region's time / steps
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -299,15 +301,13 @@ def run_ours(args):
         stop = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for s in range(args.steps):
-            ev[s][0].record(stream)
             step(s)
-            ev[s][1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     total_ms = start.elapsed_time(stop)
-    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [total_ms / args.steps]
     r = dec.result()
     assert int(r.status) == 0 and r.values_written == count
 
@@ -377,7 +377,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": statistics.mean(kern_ms),
-                         "kernel_ms_min": min(kern_ms)},
+                         "kernel_ms_note": "decode (kernels A + B) time = timed region / steps, launched "
+                                           "back to back on the current stream"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_len,
                     "d2h_bytes_per_step": 4 * count + ctypes.sizeof(_lib.MvbResult),

@@ -1634,18 +1634,27 @@ __device__ __forceinline__ void seg_complete(const SegParams& S, bool find_last_
             __syncthreads();
             if (s_seg >= 0) break;
         }
-        if (s_seg >= 0 && wid == 0) {
-            long long le = -1;
-            for (long long q = s_seg * S.seg_bytes + lane; q < (s_seg + 1) * S.seg_bytes; q += 32) {
-                const long long p = q - S.mis;
-                if (p >= 0 && p < S.len && S.in[p] < 0x80u) le = p + 1;
+        if (s_seg >= 0) {
+            // its last terminator byte: blocks of 16 bytes per thread, from the
+            // segment's end (clipped to the stream) backwards until one holds it
+            __shared__ long long s_le;
+            const long long p_lo = s_seg * S.seg_bytes - S.mis > 0 ? s_seg * S.seg_bytes - S.mis : 0;
+            long long p_hi = (s_seg + 1) * S.seg_bytes - S.mis;
+            if (p_hi > S.len) p_hi = S.len;
+            for (long long top = p_hi; top > p_lo; top -= 16ll * blockDim.x) {
+                if (threadIdx.x == 0) s_le = -1;
+                __syncthreads();
+                const long long b = top - 16ll * (threadIdx.x + 1);
+                long long le = -1;
+                for (int j = 15; j >= 0 && le < 0; --j) {
+                    const long long p = b + j;
+                    if (p >= p_lo && p < p_hi && S.in[p] < 0x80u) le = p + 1;
+                }
+                if (le >= 0) atomicMax(&s_le, le);
+                __syncthreads();
+                if (s_le >= 0) break;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const long long x = __shfl_xor_sync(0xFFFFFFFFu, le, o);
-                le = x > le ? x : le;
-            }
-            last_end_found = le > 0 ? le : 0;
+            if (threadIdx.x == 0) last_end_found = s_le > 0 ? s_le : 0;
         }
     }
     if (!S.base_in) {  // whole-stream launch: zero the segment totals (a pipelined decode's host memsets them)

@@ -10,7 +10,7 @@ dev = torch.device("cuda", 0)
 choices = [int(c) for c in os.environ["CHOICES"].split()]
 mk = {"c2": W.config2, "c1": W.config1, "all1": lambda: W.config5("all1"), "all5": lambda: W.config5("all5"),
       "p50": lambda: W.config5("p50"), "p50d": lambda: W.config5("p50", delta=True),
-      "c4s": lambda: W.config4(n=1 << 27)}
+      "c4s": lambda: W.config4(n=1 << 27), "c4": W.config4}
 for name in os.environ["CFGS"].split():
     w = mk[name]()
     per = w.encoded.size + 4 * w.count
