@@ -680,6 +680,12 @@ constexpr int kLLWinBytes = 32 * 72;  // per warp: each lane's eight 8-byte digi
 constexpr int kLaneWarpBytes = 4 * kLaneStage + 2 * kLLSlice + kLLWinBytes;  // staging + 2-slice input ring + windows
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
 static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
+static_assert(kLLWinBytes >= kLLSlice, "32-byte-lane decodes use the window area as a third input slot");
+// the sparse plain general path (<= 10 integers per lane: <= 320 per slice,
+// staged below 1296 bytes) keeps its digit windows in the top of the staging
+// buffer instead
+constexpr uint32_t kSparseWin = 4 * kLaneStage - kLLWinBytes;
+static_assert(kSparseWin >= 4 * (3 + 320) + 128, "sparse windows above the sparse staging");
 
 // Dense ranges (>= 7/8 integer per byte, i.e. mostly 1-byte integers) swizzle
 // the staging addresses: the 16-byte quad index within each 128-byte row is
@@ -1335,33 +1341,42 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             pw3 = r_word(R, qs - 4);
         }
     }
-    if (i_lo == 0 && i_hi > 0) {
-        cp_async16(rbase, pin);
-        cp_async16(rbase + 16, pin + 16);
+    // input ring of kNS slices, kNS - 1 in flight ahead of the one decoded (one
+    // commit group per slice, possibly empty)
+    constexpr int kNS = 3;
+#pragma unroll
+    for (int j = 0; j < kNS - 1; ++j) {
+        if (j >= i_lo && j < i_hi) {
+            cp_async16(rbase + kLLSlice * j, pin + kLLSlice * j);
+            cp_async16(rbase + kLLSlice * j + 16, pin + kLLSlice * j + 16);
+        }
         cp_async_commit();
     }
+    uint32_t o_rd = 0, o_wr = kLLSlice * (kNS - 1);  // ring offsets of slices i and i + kNS - 1
 #pragma unroll 1
     for (int i = 0; i < ns; ++i) {
         const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
         const bool inter = i >= i_lo && i < i_hi;                      // warp-uniform
-        const bool pfn = i + 1 >= i_lo && i + 1 < i_hi;
-        if (pfn) {
-            const uint32_t d = rbase + kLLSlice * ((i + 1) & 1);
-            cp_async16(d, pin + kLLSlice * (i + 1));
-            cp_async16(d + 16, pin + kLLSlice * (i + 1) + 16);
+        {
+            const int j = i + kNS - 1;
+            if (j >= i_lo && j < i_hi) {
+                cp_async16(rbase + o_wr, pin + static_cast<long long>(kLLSlice) * j);
+                cp_async16(rbase + o_wr + 16, pin + static_cast<long long>(kLLSlice) * j + 16);
+            }
             cp_async_commit();
+            o_wr = o_wr + kLLSlice == kLLSlice * kNS ? 0u : o_wr + kLLSlice;
         }
         const long long q0 = qs + static_cast<long long>(kLLSlice) * i + 32 * lane;
         uint4 x0, x1;
         if (inter) {
-            if (pfn) cp_async_wait<1>();
-            else cp_async_wait<0>();
-            x0 = lds128(rbase + kLLSlice * (i & 1));
-            x1 = lds128(rbase + kLLSlice * (i & 1) + 16);
+            cp_async_wait<kNS - 1>();
+            x0 = lds128(rbase + o_rd);
+            x1 = lds128(rbase + o_rd + 16);
         } else {
             x0 = r_load16(R, q0);
             x1 = r_load16(R, q0 + 16);
         }
+        o_rd = o_rd + kLLSlice == kLLSlice * kNS ? 0u : o_rd + kLLSlice;
         const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1), wp2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
         const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31), l2 = __shfl_sync(0xFFFFFFFFu, w[6], 31);
@@ -1396,7 +1411,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
         else
             carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
-                                               st_base + 4u * (a + wexcl), ring + 2u * kLLSlice + 72u * lane, carry);
+                                               st_base + 4u * (a + wexcl), st_base + kSparseWin + 72u * lane, carry);
         left = left > n_w ? left - n_w : 0u;
         if (n_w == 0) continue;
         __syncwarp();
