@@ -888,7 +888,7 @@ __device__ __forceinline__ void lane_slots_2b(uint32_t wp3, const uint32_t (&w)[
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
         const uint32_t P = __funnelshift_l(prev, w[k], 8);  // byte t = byte t-1 of the stream
-        const uint32_t cm = ((P >> 7) & 0x01010101u) * 0xFFu;  // 0xFF where byte t-1 continues
+        const uint32_t cm = prmt_sign(P, 0u, 0xBA98u);  // 0xFF where byte t-1 continues (sign-replicating prmt)
         const uint32_t X = (P & 0x7F7F7F7Fu) | ((w[k] << 7) & 0x80808080u);
         A[k] = (X & cm) | (w[k] & ~cm);
         B[k] = (w[k] >> 1) & 0x3F3F3F3Fu & cm;
