@@ -170,3 +170,61 @@ def test_lists_dense_and_sparse_around_slice_sizes(oracle, delta):
         ro, oo = oracle.decode_delta(span, counts[l], int(prev[l])) if delta else oracle.decode(span, counts[l])
         assert tuple(int(x) for x in rr[l]) == tuple(ro), l
         assert np.array_equal(got[int(int_off[l]):int(int_off[l + 1])], oo), l
+
+
+def _stream_with_long_ints_at(oracle, rng, base_lens, byte_positions, long_len):
+    """Mostly 1-2-byte integers with one long_len-byte integer ending at (or
+    just after) each requested byte position: the 1-2-byte slot path (prmt
+    candidates, its lane / slice vote) next to slices that must not take it,
+    and kernel A's 3+-byte detection (per-iteration sums plus the halo pair)."""
+    lens = list(base_lens)
+    pos = np.cumsum(lens)
+    for bp in sorted(byte_positions, reverse=True):
+        k = int(np.searchsorted(pos, bp))
+        if k < len(lens):
+            lens[k] = long_len
+    lens = np.asarray(lens)
+    return _values_of_lengths(rng, lens)
+
+
+@pytest.mark.parametrize("long_len", [3, 4, 5])
+def test_long_integers_at_lane_and_slice_seams(oracle, long_len):
+    rng = np.random.default_rng(100 + long_len)
+    base = rng.integers(1, 3, 60000)  # 1- and 2-byte integers (~90 KB)
+    # around 32-byte lane seams, 512-byte and 1 KiB slice seams, segment seams
+    seams = [32 * k + d for k in (3, 17, 31, 32, 33, 63) for d in (-2, -1, 0, 1, 2)]
+    seams += [1024 * k + d for k in (1, 2, 7, 8, 40) for d in range(-4, 5)]
+    seams += [512 * k + d for k in (3, 5) for d in (-1, 0, 1)]
+    v = _stream_with_long_ints_at(oracle, rng, base, seams, long_len)
+    enc = oracle.encode_sequence(v)
+    r, out = gpu_decode(enc, v.size)
+    assert r == (0, v.size, enc.size)
+    assert np.array_equal(out, v)
+    ro, oo = oracle.decode_delta(enc, v.size, 77)
+    rd, od = gpu_decode(enc, v.size, delta=True, prev=77)
+    assert rd == ro and np.array_equal(od, oo)
+    # the same through the device path at a misaligned input and output
+    rd2, od2 = dev_decode(__import__("torch"), __import__("torch").device("cuda", 0), enc, v.size, delta=True,
+                          prev=77, in_off=5, out_off=3)
+    assert rd2 == ro and np.array_equal(od2, oo)
+
+
+def test_two_byte_slices_dense_and_sparse_mix(oracle):
+    """Slices of only 1-byte integers (swizzled staging) and of only 2-byte
+    integers, alternating every few KiB, plus single 3-byte integers between
+    them: each slice decides its own path."""
+    rng = np.random.default_rng(808)
+    parts = []
+    for i in range(60):
+        n = int(rng.integers(500, 5000))
+        parts.append(np.ones(n, np.int64) if i % 3 == 0 else np.full(n, 2, np.int64) if i % 3 == 1
+                     else rng.integers(1, 3, n))
+        if i % 7 == 3:
+            parts.append(np.array([3], np.int64))
+    v = _values_of_lengths(rng, np.concatenate(parts))
+    enc = oracle.encode_sequence(v)
+    r, out = gpu_decode(enc, v.size)
+    assert r == (0, v.size, enc.size) and np.array_equal(out, v)
+    ro, oo = oracle.decode_delta(enc, v.size, 5)
+    rd, od = gpu_decode(enc, v.size, delta=True, prev=5)
+    assert rd == ro and np.array_equal(od, oo)
