@@ -164,7 +164,10 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
     return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
 }
 
-constexpr int kSegAChunks = 2;                     // kernel A: 16-byte chunks per lane per iteration
+#ifndef MVB_A_CHUNKS
+#define MVB_A_CHUNKS 2
+#endif
+constexpr int kSegAChunks = MVB_A_CHUNKS;          // kernel A: 16-byte chunks per lane per iteration
 constexpr int kSegASlice = 512 * kSegAChunks;      // bytes per warp iteration
 constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + the lane's bytes
 constexpr int kAStages = 4;                        // kernel A: cp.async ring depth (iterations in flight)

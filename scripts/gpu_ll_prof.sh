@@ -21,5 +21,5 @@ assert np.array_equal(out.cpu().numpy().view(np.uint32), w.expected()), "mismatc
 print("ok", d.result())
 PY
 python /tmp/seg_run.py $CFG $CHOICE > gpurun_out/ll_run.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"seg_decode|seg_totals|seg_fused" -s 4 -c 2 -o gpurun_out/prof_$TAG python /tmp/seg_run.py $CFG $CHOICE > gpurun_out/ncu_$TAG.log 2>&1; echo ncu rc=$?
+ncu --set full --clock-control none ${NCU_EXTRA:-} --import-source on -k regex:"seg_decode|seg_totals|seg_fused" -s 4 -c 2 -o gpurun_out/prof_$TAG python /tmp/seg_run.py $CFG $CHOICE > gpurun_out/ncu_$TAG.log 2>&1; echo ncu rc=$?
 cat gpurun_out/ll_run.log
