@@ -147,7 +147,12 @@ int mvb_decode_delta_lists_device(const uint8_t *in, size_t in_len, const unsign
 /* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream
  * (and of decode_scalar / decode_delta_scalar, which have identical results).
  * Return value: the DecodeStatus (>= 0) or a negative MVB_ERR_*; *res (may be
- * NULL) receives the full DecodeResult. */
+ * NULL) receives the full DecodeResult.  Strict-mode streams of >= 4 MB are
+ * decoded in chunks that overlap the host->device copy of later chunks, the
+ * decode and the device->host copy of earlier chunks' values (pinned buffers
+ * make the copies asynchronous; pageable ones still work).  Only
+ * out[0 .. values_written) (and, after a malformed integer, possibly a few
+ * more decoded slots) is written. */
 int mvb_decode_stream(const uint8_t *in, size_t in_len, size_t count, uint32_t *out, int mode,
                       mvb_result *res);
 int mvb_decode_delta_stream(const uint8_t *in, size_t in_len, size_t count, uint32_t prev,
