@@ -1292,13 +1292,19 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
             ob[i] = v;
         }
     }
-    for (uint32_t i = i0 + 4 * lane; i < i1; i += 128) {
+    // whole quads: a shared address and a global pointer that both advance by
+    // one warp-row per iteration (no per-store 64-bit index arithmetic)
+    uint32_t i = i0 + 4 * lane;
+    uint32_t sa = st_base + 4u * i;
+    uint4* dst = reinterpret_cast<uint4*>(ob + i);
+#pragma unroll 4
+    for (; i < i1; i += 128, sa += 512u, dst += 32) {
         uint4 v;
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "r"(stg_addr<kSwz>(st_base + 4u * i))
+                     : "r"(stg_addr<kSwz>(sa))
                      : "memory");
-        *reinterpret_cast<uint4*>(ob + i) = v;
+        *dst = v;
     }
 }
 
