@@ -680,10 +680,10 @@ constexpr int kLLSlice = 1024;                     // bytes per slice: 32 lanes 
 constexpr int kLaneGroup = 2;                      // (V/EP-sized staging: 2 x 512 integers)
 constexpr int kLaneStage = kLaneGroup * 512 + 32;  // staging words per warp (+ alignment), whole 128-byte rows
 constexpr int kLLWinBytes = 32 * 72;  // per warp: each lane's eight 8-byte digit windows (72-byte stride: 2 banks apart)
-constexpr int kLaneWarpBytes = 4 * kLaneStage + 2 * kLLSlice + kLLWinBytes;  // staging + 2-slice input ring + windows
+constexpr int kLaneWarpBytes = 4 * kLaneStage + 3 * kLLSlice;  // staging (+ sparse windows) + 3-slice input ring
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
 static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
-static_assert(kLLWinBytes >= kLLSlice, "32-byte-lane decodes use the window area as a third input slot");
+
 // the sparse plain general path (<= 10 integers per lane: <= 320 per slice,
 // staged below 1296 bytes) keeps its digit windows in the top of the staging
 // buffer instead
