@@ -665,6 +665,9 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 // integers, the end of integer limit-1).  Delta: in-lane running sums stay in
 // registers, the warp scan of the lane totals adds the offsets before the
 // stores.
+#ifndef MVB_GEN_INLINE
+#define MVB_GEN_INLINE __noinline__  // the 32-byte-lane general path (rare) as a call
+#endif
 #ifndef MVB_DELTA32
 #define MVB_DELTA32 1  // delta stream decodes on 32-byte lanes too (0: 16-byte lanes, two slices per staging group)
 #endif
@@ -1242,7 +1245,7 @@ __device__ __forceinline__ void gen_sparse_plain(uint32_t wp3, const uint4 x0, c
 // halves): strict checks, then the general slots.  Delta: both halves' sums
 // first (the output order is lane-major), one warp scan, then the stores.
 template <bool kDelta, bool kSwz>
-__device__ __noinline__ uint32_t ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
+__device__ MVB_GEN_INLINE uint32_t ll_slice_gen(const ByteRange& R, long long q0, const uint4 x0, const uint4 x1,
                                           uint32_t wp2, uint32_t wp3, uint32_t T32, uint32_t inr32, uint32_t n_w,
                                           uint32_t wexcl, unsigned long long rs, unsigned long long limit,
                                           const RangeSink& K, uint32_t sp, uint32_t win, uint32_t carry) {
