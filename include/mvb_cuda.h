@@ -142,6 +142,20 @@ int mvb_decode_delta_lists_device(const uint8_t *in, size_t in_len, const unsign
                                   size_t n_lists, const unsigned *order, uint32_t *out, int mode,
                                   mvb_result *results, void *ws, size_t ws_bytes, mvb_stream_t stream);
 
+/* Host-pointer batched decode (the same lists, offsets and results as the
+ * _device entry points above, all in host memory).  Synchronous.  The lists
+ * are cut into contiguous sub-batches whose host->device copies, decodes and
+ * device->host copies overlap (each sub-batch's output range is known from
+ * int_off, so no host round trip sits between them); pinned buffers make the
+ * copies asynchronous.  Strict mode only.  Returns 0 or a negative MVB_ERR_*;
+ * the per-list statuses are in results[] (may be NULL). */
+int mvb_decode_lists(const uint8_t *in, size_t in_len, const unsigned long long *byte_off,
+                     const unsigned long long *int_off, size_t n_lists, uint32_t *out, int mode,
+                     mvb_result *results);
+int mvb_decode_delta_lists(const uint8_t *in, size_t in_len, const unsigned long long *byte_off,
+                           const unsigned long long *int_off, const uint32_t *prev, size_t n_lists,
+                           uint32_t *out, int mode, mvb_result *results);
+
 /* ------------------------------------------------------------ host drop-ins */
 
 /* Synchronous host-pointer equivalents of decode_stream / decode_delta_stream

@@ -24,6 +24,8 @@ EXPORTS = (
     "mvb_shard_carry_device",
     "mvb_decode_lists_device",
     "mvb_decode_delta_lists_device",
+    "mvb_decode_lists",
+    "mvb_decode_delta_lists",
     "mvb_encode_workspace_bytes",
     "mvb_encode_sequence_device",
     "mvb_encode_deltas_device",
@@ -76,6 +78,10 @@ def _declare(lib):
     lib.mvb_decode_lists_device.restype = i32
     lib.mvb_decode_delta_lists_device.argtypes = [vp, sz, vp, vp, vp, sz, vp, vp, i32, vp, vp, sz, vp]
     lib.mvb_decode_delta_lists_device.restype = i32
+    lib.mvb_decode_lists.argtypes = [vp, sz, vp, vp, sz, vp, i32, vp]
+    lib.mvb_decode_lists.restype = i32
+    lib.mvb_decode_delta_lists.argtypes = [vp, sz, vp, vp, vp, sz, vp, i32, vp]
+    lib.mvb_decode_delta_lists.restype = i32
     lib.mvb_encode_workspace_bytes.argtypes = [sz]
     lib.mvb_encode_workspace_bytes.restype = sz
     lib.mvb_encode_sequence_device.argtypes = [vp, sz, vp, vp, vp, sz, vp]

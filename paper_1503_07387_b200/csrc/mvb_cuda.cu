@@ -461,6 +461,15 @@ struct HostCtx {
     size_t ws_cap = 0;
     mvb_result* d_res = nullptr;
     unsigned long long* d_base = nullptr;  // pipelined decode: [count, sum] before each chunk
+    // batched host decode: offsets, prevs and per-list results on the device
+    unsigned long long* d_bo = nullptr;
+    size_t bo_cap = 0;
+    unsigned long long* d_io = nullptr;
+    size_t io_cap = 0;
+    uint32_t* d_prev = nullptr;
+    size_t prev_cap = 0;
+    mvb_result* d_lres = nullptr;
+    size_t lres_cap = 0;
     // pinned, device-mapped: per-chunk integer totals and the DecodeResult the
     // final kernel writes (read by the host once the kernel's event completed)
     unsigned long long* h_tot = nullptr;
@@ -762,9 +771,94 @@ int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byt
                : lists_device_t<Delta, 1>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev,
                                           ws, ws_bytes, s);
 }
+// Batched host decode (mvb_decode_lists / mvb_decode_delta_lists): contiguous
+// sub-batches of lists, about g_pipe_chunk x 4 bytes or in_len / 16 each (at
+// most 64); sub-batch b's bytes, offsets and prevs go up on the H2D stream,
+// its lists kernel waits for them, and the D2H of its output range
+// [int_off[l0], int_off[l1]) and results waits for the kernel -- all queued up
+// front, the three streams overlap.
+template <bool Delta>
+int lists_host(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+               const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, uint32_t* out, int mode,
+               mvb_result* results) {
+    if (n_lists == 0) return 0;
+    if (byte_off == nullptr || int_off == nullptr || (in == nullptr && in_len > 0)) return MVB_ERR_INVALID_ARG;
+    if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;
+    const unsigned long long n_out = int_off[n_lists];
+    if (n_out > 0 && out == nullptr) return MVB_ERR_INVALID_ARG;
+    HostCtx& c = g_ctx;
+    if (!c.init()) return MVB_ERR_CUDA;
+    if (!HostCtx::grow(c.d_in, c.in_cap, in_len, false) ||
+        !HostCtx::grow(c.d_out, c.out_cap, static_cast<size_t>(n_out) * 4, false) ||
+        !HostCtx::grow(c.d_ws, c.ws_cap, mvb_workspace_bytes(0), true) ||
+        !HostCtx::grow(c.d_bo, c.bo_cap, (n_lists + 1) * 8, false) ||
+        !HostCtx::grow(c.d_io, c.io_cap, (n_lists + 1) * 8, false) ||
+        !HostCtx::grow(c.d_lres, c.lres_cap, n_lists * sizeof(mvb_result), false) ||
+        (prev && !HostCtx::grow(c.d_prev, c.prev_cap, n_lists * 4, false)))
+        return MVB_ERR_CUDA;
+    // sub-batches [lb[b], lb[b + 1])
+    size_t lb[65];
+    int nb = 0;
+    {
+        const unsigned long long total = byte_off[n_lists] - byte_off[0];
+        unsigned long long target = g_pipe_grow ? std::max<unsigned long long>(4ull * g_pipe_chunk, total / 16)
+                                                : std::max<unsigned long long>(g_pipe_chunk, 1);
+        if (total / target > 63) target = total / 63 + 1;
+        lb[0] = 0;
+        size_t l = 0;
+        while (l < n_lists) {
+            const unsigned long long start = byte_off[l];
+            size_t e = l + 1;
+            while (e < n_lists && byte_off[e] - start < target) ++e;
+            if (nb == 63) e = n_lists;
+            lb[++nb] = e;
+            l = e;
+        }
+    }
+    for (int b = 0; b < nb; ++b) {
+        const size_t l0 = lb[b], l1 = lb[b + 1];
+        const size_t b0 = static_cast<size_t>(std::min<unsigned long long>(byte_off[l0], in_len));
+        const size_t b1 = static_cast<size_t>(std::min<unsigned long long>(byte_off[l1], in_len));
+        if (b1 > b0 && cudaMemcpyAsync(c.d_in + b0, in + b0, b1 - b0, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (cudaMemcpyAsync(c.d_bo + l0, byte_off + l0, (l1 - l0 + 1) * 8, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess ||
+            cudaMemcpyAsync(c.d_io + l0, int_off + l0, (l1 - l0 + 1) * 8, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (prev && cudaMemcpyAsync(c.d_prev + l0, prev + l0, (l1 - l0) * 4, cudaMemcpyHostToDevice, c.h2d) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (cudaEventRecord(c.ev_in[b], c.h2d) != cudaSuccess) return MVB_ERR_CUDA;
+        if (cudaStreamWaitEvent(c.stream, c.ev_in[b], 0) != cudaSuccess) return MVB_ERR_CUDA;
+        const int rc = lists_device<Delta>(c.d_in, in_len, c.d_bo + l0, c.d_io + l0, prev ? c.d_prev + l0 : nullptr,
+                                           l1 - l0, nullptr, n_out ? c.d_out : nullptr, mode, c.d_lres + l0, c.d_ws,
+                                           c.ws_cap, c.stream);
+        if (rc) return rc;
+        if (cudaEventRecord(c.ev_dec[b], c.stream) != cudaSuccess) return MVB_ERR_CUDA;
+        if (cudaStreamWaitEvent(c.d2h, c.ev_dec[b], 0) != cudaSuccess) return MVB_ERR_CUDA;
+        const unsigned long long o0 = int_off[l0], o1 = int_off[l1];
+        if (o1 > o0 && cudaMemcpyAsync(out + o0, c.d_out + o0, static_cast<size_t>(o1 - o0) * 4, cudaMemcpyDeviceToHost,
+                                       c.d2h) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        if (results && cudaMemcpyAsync(results + l0, c.d_lres + l0, (l1 - l0) * sizeof(mvb_result),
+                                       cudaMemcpyDeviceToHost, c.d2h) != cudaSuccess)
+            return MVB_ERR_CUDA;
+    }
+    return cudaStreamSynchronize(c.d2h) == cudaSuccess && cudaStreamSynchronize(c.stream) == cudaSuccess ? 0
+                                                                                                   : MVB_ERR_CUDA;
+}
 }  // namespace
 
 extern "C" {
+
+int mvb_decode_lists(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                     const unsigned long long* int_off, size_t n_lists, uint32_t* out, int mode, mvb_result* results) {
+    return lists_host<false>(in, in_len, byte_off, int_off, nullptr, n_lists, out, mode, results);
+}
+
+int mvb_decode_delta_lists(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+                           const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, uint32_t* out,
+                           int mode, mvb_result* results) {
+    return lists_host<true>(in, in_len, byte_off, int_off, prev, n_lists, out, mode, results);
+}
 
 int mvb_decode_lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
                             const unsigned long long* int_off, size_t n_lists, const unsigned* order, uint32_t* out,

@@ -280,6 +280,40 @@ def _decode(inp, count, prev, out, options, delta: bool):
     return DecodeResult(DecodeStatus(res.status), int(res.values_written), int(res.bytes_consumed))
 
 
+def decode_lists(inp, byte_offsets, int_offsets, out, prev=None, delta: bool = True, results: bool = True):
+    """Batched posting lists from host memory (mvb_decode[_delta]_lists): list
+    l is inp[byte_offsets[l]:byte_offsets[l+1]] holding int_offsets[l+1] -
+    int_offsets[l] integers, decoded (delta from prev[l], default 0) into
+    out[int_offsets[l]:...] -- as one decode[_delta]_stream call per list
+    (tools/bench/runner.cpp:28-61) would, in one pipelined batch.  Returns the
+    per-list DecodeResults as an (n, 3) uint64 array (status, values_written,
+    bytes_consumed), or None if ``results`` is False."""
+    src = _u8(inp)
+    bo = np.ascontiguousarray(byte_offsets, np.uint64)
+    io = np.ascontiguousarray(int_offsets, np.uint64)
+    n = int(bo.size) - 1
+    if io.size != bo.size:
+        raise MvbError("byte_offsets and int_offsets need the same length (n_lists + 1)")
+    if not (isinstance(out, np.ndarray) and out.dtype in (np.uint32, np.int32) and out.flags.c_contiguous):
+        raise MvbError("output must be a C-contiguous numpy uint32 array")
+    if n > 0 and out.size < int(io[-1]):
+        raise MvbError("output array smaller than int_offsets[-1]")
+    pv = None if prev is None else np.ascontiguousarray(prev, np.uint32)
+    res = np.zeros((max(n, 1), 3), np.uint64) if results else None
+    L = _lib.lib()
+    if delta:
+        rc = L.mvb_decode_delta_lists(_ptr(src), src.size, _ptr(bo), _ptr(io), _ptr(pv) if pv is not None else None,
+                                      n, _ptr(out), 0, _ptr(res) if res is not None else None)
+    else:
+        rc = L.mvb_decode_lists(_ptr(src), src.size, _ptr(bo), _ptr(io), n, _ptr(out), 0,
+                                _ptr(res) if res is not None else None)
+    _check(rc)
+    if res is None:
+        return None
+    res[:, 0] &= 0xFFFFFFFF
+    return res[:n]
+
+
 def decode_stream(inp, count=None, out=None, options: Union[DecodeOptions, DecodeMode, int, None] = None):
     """Decodes exactly ``count`` integers of ``inp`` into ``out`` (decode.hpp:44-47).
 

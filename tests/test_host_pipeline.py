@@ -110,3 +110,63 @@ def test_pipelined_default_threshold_full_config2():
         r, out = host_decode(w.encoded, w.count, delta=True, prev=w.prev)
         assert r == (0, w.count, w.encoded.size)
         assert np.array_equal(out, exp)
+
+
+def _lists_batch(oracle, seed, n_lists=400):
+    """Lists as in test_batched_lists_equal_per_list_oracle: empty ones,
+    count-limited, truncated and malformed ones, an unaligned first start."""
+    rng = np.random.default_rng(seed)
+    parts, counts, prevs = [], [], []
+    for l in range(n_lists):
+        n = int(rng.integers(0, 3000)) if l % 7 else int(rng.integers(0, 4))
+        v = W.mixed_values(n, l + 11) if n else np.zeros(0, np.uint32)
+        e = oracle.encode_sequence(v) if n else np.zeros(0, np.uint8)
+        cnt = n
+        if l % 11 == 3 and n > 2:
+            cnt = n - 2
+        if l % 13 == 5 and e.size > 3:
+            e = e[:-1]
+        if l % 17 == 9 and e.size > 40:
+            e = e.copy()
+            e[20:26] = 0x80
+        parts.append(e)
+        counts.append(cnt)
+        prevs.append(int(rng.integers(0, 1 << 32)))
+    byte_off = np.zeros(n_lists + 1, np.uint64)
+    byte_off[1:] = np.cumsum([p.size for p in parts])
+    int_off = np.zeros(n_lists + 1, np.uint64)
+    int_off[1:] = np.cumsum(counts)
+    data = np.concatenate([np.zeros(5, np.uint8)] + parts)
+    byte_off += 5
+    return data, byte_off, int_off, parts, counts, np.array(prevs, np.uint32)
+
+
+@pytest.mark.parametrize("delta", [True, False])
+@pytest.mark.parametrize("grow", [False, True])
+def test_host_lists_equal_per_list_oracle(oracle, delta, grow):
+    """mvb_decode[_delta]_lists (host pointers, sub-batches pipelined; with
+    1-byte sub-batch targets every list up to the 63rd is its own sub-batch)
+    against one oracle decode per list."""
+    data, byte_off, int_off, parts, counts, prevs = _lists_batch(oracle, 5 if delta else 6)
+    _lib.set_host_pipeline(0, 1, grow=grow)
+    try:
+        out = np.full(int(int_off[-1]) + 4, 0xFFFFFFFF, np.uint32)
+        res = mvb.decode_lists(data, byte_off, int_off, out, prev=prevs if delta else None, delta=delta)
+    finally:
+        _lib.set_host_pipeline()
+    for l in range(len(parts)):
+        span = data[int(byte_off[l]):int(byte_off[l + 1])]
+        ro, oo = oracle.decode_delta(span, counts[l], int(prevs[l])) if delta else oracle.decode(span, counts[l])
+        assert tuple(int(x) for x in res[l]) == tuple(ro), (l, res[l], ro)
+        k = ro[1]
+        np.testing.assert_array_equal(out[int(int_off[l]):int(int_off[l]) + k], oo[:k], err_msg=f"list {l}")
+    assert out[int(int_off[-1]):].tolist() == [0xFFFFFFFF] * 4
+
+
+def test_host_lists_config3_checksum():
+    """BASELINE config 3 through the host batched entry (default sub-batches)."""
+    w = W.config3()
+    out = np.zeros(w.count, np.uint32)
+    res = mvb.decode_lists(w.encoded, w.byte_offsets, w.int_offsets, out, delta=True)
+    assert (res[:, 0] == 0).all()
+    assert np.array_equal(out, w.expected())
