@@ -665,6 +665,12 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 // integers, the end of integer limit-1).  Delta: in-lane running sums stay in
 // registers, the warp scan of the lane totals adds the offsets before the
 // stores.
+#ifndef MVB_PATH_STATS
+#define MVB_PATH_STATS 0  // (profiling builds: count 32-byte-lane slices per path)
+#endif
+#if MVB_PATH_STATS
+__device__ unsigned long long mvb_path_counts[4];  // 2-byte, fast, general interior, general edge
+#endif
 #ifndef MVB_GEN_INLINE
 #define MVB_GEN_INLINE __noinline__  // the 32-byte-lane general path (rare) as a call
 #endif
@@ -1415,8 +1421,11 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         const unsigned long long run2 = pair & 0xFFFFFFFFCull;              // a 3+-byte integer ends in 0..31
         const unsigned long long run4 = pair & (pair >> 2) & 0x1FFFFFFFFull;  // a 5+-byte integer ends in 0..31
         const bool ok_range = inter && n_w < left;
-        const unsigned vote = __ballot_sync(0xFFFFFFFFu, run2 != 0) | (__ballot_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
+        const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
         if (n_w) last_i = i;
+#if MVB_PATH_STATS
+        if (lane == 0) atomicAdd(&mvb_path_counts[(ok_range && vote == 0) ? 0 : (ok_range && !(vote & 2u)) ? 1 : inter ? 2 : 3], 1ull);
+#endif
         if (ok_range && vote == 0)
             lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
         else if (ok_range && !(vote & 2u))
@@ -1531,7 +1540,7 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             const uint32_t run2 = pair & 0xFFFFCu;     // a 3+-byte integer ends in 0..15
             const uint32_t run4 = pair & (pair >> 2);  // a 5+-byte integer ends in 0..15
             const bool ok_range = inter && n_w < left;
-            const unsigned vote = __ballot_sync(0xFFFFFFFFu, run2 != 0) | (__ballot_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
+            const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
             if (n_w) last_i = i;
             if (ok_range && vote == 0) {
                 const uint32_t wv[4] = {w0, w1, w2, w3};

@@ -994,6 +994,15 @@ int mvbx_set_trace_b(unsigned long long* buf) {
 }
 #endif
 
+#if MVB_PATH_STATS
+// Internal profiling entry (path-stats builds only): slices per path since the last call.
+int mvbx_path_counts(unsigned long long* out4) {
+    if (cudaMemcpyFromSymbol(out4, mvbk::mvb_path_counts, 4 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    return cudaMemcpyToSymbol(mvbk::mvb_path_counts, z, sizeof z) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
