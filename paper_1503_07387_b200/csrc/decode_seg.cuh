@@ -1542,6 +1542,9 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             const bool ok_range = inter && n_w < left;
             const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
             if (n_w) last_i = i;
+#if MVB_PATH_STATS
+            if (lane == 0) atomicAdd(&mvb_path_counts[(ok_range && vote == 0) ? 0 : (ok_range && !(vote & 2u)) ? 1 : inter ? 2 : 3], 1ull);
+#endif
             if (ok_range && vote == 0) {
                 const uint32_t wv[4] = {w0, w1, w2, w3};
                 lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16, st_base + 4u * (a + n_g + wexcl), carry);
