@@ -237,6 +237,26 @@ __device__ __forceinline__ uint32_t words_digit_sum_hi(const uint32_t (&w)[kW]) 
     return sum;
 }
 
+// The weight correction of words_digit_sum_hi when no byte follows three
+// continuation bytes (integers of at most 3 bytes, e.g. c4's rare long gaps):
+// a byte after exactly two continuation bytes weighs 2^14 instead of the 128
+// the first pass gave it.  long4 collects the bytes that follow three (the
+// caller then falls back to words_digit_sum_hi).
+template <int kW>
+__device__ __forceinline__ uint32_t words_digit_sum_hi3(const uint32_t (&w)[kW], uint32_t& long4) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 2; k < kW; ++k) {
+        const uint32_t ck = w[k] & 0x80808080u, cp = w[k - 1] & 0x80808080u;
+        const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+        const uint32_t c3 = __funnelshift_l(cp, ck, 24);
+        const uint32_t cc = c1 & c2;
+        long4 |= cc & c3;
+        s = __dp4a(w[k] & 0x7F7F7F7Fu, cc >> 7, s);
+    }
+    return s * (16384u - 128u);
+}
+
 template <bool kDelta>
 __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_begin, long long it_end, int lane,
                                                uint32_t ring) {
@@ -358,7 +378,11 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
             // the halo): an integer of 3..5 bytes, whose later bytes need the
             // weights 2^14 / 2^21 / 2^28
             const bool pair = sb != (nc << 7) || ((w[1] & (w[1] << 8)) >> 31);
-            if (__any_sync(0xFFFFFFFFu, pair)) sum += words_digit_sum_hi(w);
+            if (__any_sync(0xFFFFFFFFu, pair)) {
+                uint32_t long4 = 0;
+                const uint32_t c3 = words_digit_sum_hi3(w, long4);
+                sum += __any_sync(0xFFFFFFFFu, long4 != 0) ? words_digit_sum_hi(w) : c3;
+            }
         }
         if (--to_flush == 0 || it + 1 == n_it) {  // leaving segment s: flush
             const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, tcount);
