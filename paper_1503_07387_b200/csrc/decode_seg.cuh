@@ -1082,16 +1082,33 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w
             pv = w[k];
         }
         if (__any_sync(0xFFFFFFFFu, hic)) {  // bytes after 2 or 3 continuation bytes: 2^14 / 2^21, not 128
+            // first the cheap case (3-byte integers only: one dp4a per word); a
+            // byte after three continuation bytes (a 4-byte integer) in any lane
+            // takes the full correction
+            uint32_t d3 = 0, long4 = 0;
             pv = wp3;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t ck = w[k] & 0x80808080u, cp = pv & 0x80808080u;
-                const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
-                const uint32_t c3 = __funnelshift_l(cp, ck, 24);
-                const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
-                S += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3), 0u) << 14;
-                S -= __dp4a(b, cc >> 7, 0u) << 7;
+                const uint32_t cc = __funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16);
+                long4 |= cc & __funnelshift_l(cp, ck, 24);
+                d3 = __dp4a(w[k] & 0x7F7F7F7Fu, cc >> 7, d3);
                 pv = w[k];
+            }
+            if (!__any_sync(0xFFFFFFFFu, long4 != 0)) {
+                S += d3 * (16384u - 128u);
+            } else {
+                pv = wp3;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t ck = w[k] & 0x80808080u, cp = pv & 0x80808080u;
+                    const uint32_t c1 = __funnelshift_l(cp, ck, 8), c2 = __funnelshift_l(cp, ck, 16);
+                    const uint32_t c3 = __funnelshift_l(cp, ck, 24);
+                    const uint32_t cc = c1 & c2, b = w[k] & 0x7F7F7F7Fu;
+                    S += __dp4a(b, ((cc & ~c3) >> 7) | (cc & c3), 0u) << 14;
+                    S -= __dp4a(b, cc >> 7, 0u) << 7;
+                    pv = w[k];
+                }
             }
         }
         const uint32_t own =
