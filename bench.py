@@ -491,10 +491,22 @@ def run_sharded(args):
     peak, peak_kind = load_peaks()
 
     # end to end: H2D of this rank's byte range from pinned memory, the pass,
-    # D2H of its decoded integers, every step
-    h_out = torch.empty(max(sh.bound, 1), dtype=torch.int32).pin_memory()
+    # D2H of its decoded integers, every step.  One GPU: the whole stream through
+    # the host-pointer drop-in (mvb_decode_delta_stream, pipelined chunks)
+    h_out = torch.empty(max(sh.bound, 1) if world > 1 else max(w.count, 1), dtype=torch.int32).pin_memory()
+    from paper_1503_07387_b200 import _lib
+    Lh = _lib.lib()
+    e2e_api = "DeviceShard.run (pre-pass, all-gather, carry, decode) with pinned H2D/D2H"
+    if world == 1:
+        e2e_api = "mvb_decode_delta_stream (host pointers, pinned, pipelined chunks)"
+        res_h = _lib.MvbResult()
 
     def e2e_step():
+        if world == 1:
+            rc = Lh.mvb_decode_delta_stream(h_buf.data_ptr(), L, w.count, w.prev, h_out.data_ptr(), 0,
+                                            ctypes.byref(res_h))
+            assert rc == 0 and res_h.values_written == w.count, (rc, res_h.values_written)
+            return
         buf.copy_(h_buf, non_blocking=True)
         sh.run()
         h_out[:n_local].copy_(sh.out[:n_local], non_blocking=True)
@@ -540,8 +552,7 @@ def run_sharded(args):
                          "kernel_ms_min": min(kern_ms), "kernel": "decode of rank 0's shard"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_buf.numel()),
-                    "d2h_bytes_per_step": 4 * n_local,
-                    "api": "DeviceShard.run (pre-pass, all-gather, carry, decode) with pinned H2D/D2H"},
+                    "d2h_bytes_per_step": 4 * (n_local if world > 1 else w.count), "api": e2e_api},
             "gpu_launches": args.steps * sh.launches_per_pass,
             "clocks": clk.summary(),
         }
