@@ -461,6 +461,23 @@ __device__ __forceinline__ void sink_count_end(const RangeSink& K, long long pos
     else *K.count_end = pos;
 }
 
+// Bits 0..3: which of the 4 bytes before q0 lie before the range end (bytes at
+// or past it read as 0x80 and must not count as continuation bytes).
+__device__ __forceinline__ uint32_t halo_in_range(const ByteRange& R, long long q0) {
+    const long long n = R.hi - (q0 - 4);
+    return n >= 4 ? 0xFu : n <= 0 ? 0u : (1u << n) - 1u;
+}
+
+// The end of the slice's integer of slice rank r (the lane holding it records
+// it): ends = the lane's in-range terminator bits, wexcl / n_own its rank range.
+__device__ __forceinline__ void slice_count_end(const ByteRange& R, const RangeSink& K, long long q0, uint32_t ends,
+                                                uint32_t r, uint32_t wexcl, uint32_t n_own) {
+    if (r < wexcl || r >= wexcl + n_own) return;
+    uint32_t m = ends;
+    for (uint32_t k = r - wexcl; k > 0; --k) m &= m - 1;
+    sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
+}
+
 // What a range decode returns (identical in every lane).
 struct RangeOut {
     long long last_end;  // -1 if the range holds no integer
@@ -1381,12 +1398,6 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     }
     const uint8_t* const pin = R.ab + qs + 32 * lane;  // this lane's bytes of slice 0
     const uint32_t rbase = ring + 32u * lane;
-    // integers that may still be stored before `limit` (clamped): a slice with fewer takes the fast path
-    uint32_t left;
-    {
-        const unsigned long long r = limit > base ? limit - base : 0ull;
-        left = r > 0x7FFFFFFFull ? 0x7FFFFFFFu : static_cast<uint32_t>(r);
-    }
     unsigned long long run = base;  // output index of the slice's first integer
     int last_i = -1;                // the last slice holding an integer (warp-uniform)
     uint32_t pw2 = 0, pw3 = 0;      // lane 0: the 8 bytes before the slice
@@ -1457,24 +1468,35 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
         const uint32_t wexcl = incl - n_own;
         // four continuation bytes in a row anywhere in positions -4..31
-        const unsigned long long C = ((static_cast<unsigned long long>(~T32) << 4) | (~hibits4(~wp3) & 0xFu));
+        // a tail slice (bytes past the range end only, read as 0x80: never
+        // terminators) may take the fast paths too (delta: the 2-byte one only --
+        // the fast path's lane sum assumes a terminator in the lane's last word);
+        // its vote counts continuation bytes inside the range only
+        const bool tail = !inter && qs + static_cast<long long>(kLLSlice) * i >= R.lo;
+        const unsigned long long C = (static_cast<unsigned long long>(~T32 & inr32) << 4) |
+                                     (~hibits4(~wp3) & (inter ? 0xFu : halo_in_range(R, q0)));
         const unsigned long long pair = C & (C >> 1);                       // bit j: positions j-4, j-3 continue
         const unsigned long long run2 = pair & 0xFFFFFFFFCull;              // a 3+-byte integer ends in 0..31
         const unsigned long long run4 = pair & (pair >> 2) & 0x1FFFFFFFFull;  // a 5+-byte integer ends in 0..31
-        const bool ok_range = inter && n_w < left;
         const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
+        const bool take2 = (inter || tail) && vote == 0;
+        const bool takef = !take2 && (inter || (tail && !kDelta)) && !(vote & 2u);
         if (n_w) last_i = i;
 #if MVB_PATH_STATS
-        if (lane == 0) atomicAdd(&mvb_path_counts[(ok_range && vote == 0) ? 0 : (ok_range && !(vote & 2u)) ? 1 : inter ? 2 : 3], 1ull);
+        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : takef ? 1 : inter ? 2 : 3], 1ull);
 #endif
-        if (ok_range && vote == 0)
-            lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
-        else if (ok_range && !(vote & 2u))
-            lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
-        else
+        if (take2 || takef) {
+            if (take2)
+                lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+            else
+                lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+            // the slice holds integer limit-1: record its end (stores past limit are
+            // dropped by the copy-out)
+            if (run < limit && run + n_w >= limit)
+                slice_count_end(R, K, q0, T32 & inr32, static_cast<uint32_t>(limit - 1 - run), wexcl, n_own);
+        } else
             carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
                                                st_base + 4u * (a + wexcl), st_base + kSparseWin + 72u * lane, carry);
-        left = left > n_w ? left - n_w : 0u;
         if (n_w == 0) continue;
         __syncwarp();
         stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
@@ -1576,22 +1598,37 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             }
             const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
             const uint32_t wexcl = incl - n_own;
-            const uint32_t C20 = ~(hibits4(~wp3) | (T16 << 4)) & 0xFFFFFu;  // continuation bytes, positions -4..15
+            // a tail slice (bytes past the range end only, read as 0x80: never
+            // terminators) may take the 2-byte path too; its vote counts
+            // continuation bytes inside the range only
+            const bool tail = !inter && qs + static_cast<long long>(kSegSlice) * i >= R.lo;
+            const uint32_t C20 =
+                ~(hibits4(~wp3) | (T16 << 4)) &
+                (inter ? 0xFFFFFu
+                       : (inr16 << 4) | halo_in_range(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane));
             const uint32_t pair = C20 & (C20 >> 1);  // bit j: positions j-4, j-3 both continue
             const uint32_t run2 = pair & 0xFFFFCu;     // a 3+-byte integer ends in 0..15
             const uint32_t run4 = pair & (pair >> 2);  // a 5+-byte integer ends in 0..15
-            const bool ok_range = inter && n_w < left;
             const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
+            const bool take2 = (inter || tail) && vote == 0;
+            const bool takef = !take2 && inter && !(vote & 2u);
             if (n_w) last_i = i;
 #if MVB_PATH_STATS
-            if (lane == 0) atomicAdd(&mvb_path_counts[(ok_range && vote == 0) ? 0 : (ok_range && !(vote & 2u)) ? 1 : inter ? 2 : 3], 1ull);
+            if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : takef ? 1 : inter ? 2 : 3], 1ull);
 #endif
-            if (ok_range && vote == 0) {
-                const uint32_t wv[4] = {w0, w1, w2, w3};
-                lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16, st_base + 4u * (a + n_g + wexcl), carry);
-            } else if (ok_range && !(vote & 2u))
-                lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
-            else
+            if (take2 || takef) {
+                if (take2) {
+                    const uint32_t wv[4] = {w0, w1, w2, w3};
+                    lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16, st_base + 4u * (a + n_g + wexcl), carry);
+                } else {
+                    lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
+                }
+                // the slice holds integer limit-1: record its end (stores past limit are
+                // dropped by the copy-out)
+                if (left > 0 && n_w >= left)
+                    slice_count_end(R, K, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, T16 & inr16,
+                                    left - 1, wexcl, n_own);
+            } else
                 carry = ll_slice_gen16<kDelta, kSwz>(R, qs + static_cast<long long>(kSegSlice) * i + 16 * lane, w0,
                                                      w1, w2, w3, wp3, T16, inr16, n_own, n_w, wexcl, run + n_g, limit,
                                                      K, st_base + 4u * (a + n_g + wexcl), carry);
