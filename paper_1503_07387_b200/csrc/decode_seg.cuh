@@ -164,6 +164,9 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
     return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
 }
 
+#ifndef MVB_A_MINB
+#define MVB_A_MINB 1  // kernel A: minimum resident CTAs per SM (register cap)
+#endif
 #ifndef MVB_A_CHUNKS
 #define MVB_A_CHUNKS 2
 #endif
@@ -184,7 +187,7 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long s_b
                                                uint32_t ring);
 
 template <bool kDelta>
-__global__ void __launch_bounds__(kSegThreads) vbyte_seg_totals(SegParams S) {
+__global__ void __launch_bounds__(kSegThreads, MVB_A_MINB) vbyte_seg_totals(SegParams S) {
     const int lane = threadIdx.x & 31;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -712,6 +715,12 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 #if MVB_PATH_STATS
 __device__ unsigned long long mvb_path_counts[4];  // 2-byte, fast, general interior, general edge
 #endif
+#ifndef MVB_FAST5
+#define MVB_FAST5 1  // plain slices with canonical 5-byte integers on the fast path
+#endif
+#ifndef MVB_F5_MIN
+#define MVB_F5_MIN 256  // ... when the slice holds at least this many integers (sparser: the general path's per-integer loop)
+#endif
 #ifndef MVB_GEN_INLINE
 #define MVB_GEN_INLINE __noinline__  // the 32-byte-lane general path (rare) as a call
 #endif
@@ -1076,9 +1085,14 @@ __device__ __noinline__ uint32_t ll_slice_gen16(const ByteRange& R, long long q0
 // the FMA pipe, leaving the (half-rate) ALU pipe the predicate, the select
 // and the funnel shift.  Delta: the lane's exclusive prefix comes first (SWAR
 // digit-weight sum, warp scan), then each slot stores the running sum.
-template <bool kDelta, bool kSwz>
+// kF5 (plain only): F5 marks the bytes ending a 5-byte integer (the four bytes
+// before continue; the vote has checked that each is a terminator < 0x10).  The
+// m chain wraps to 0 there; such a slot takes the window's bits [7t, 7t + 32)
+// instead: the four bytes before at bits 0..27, the fifth byte's low 4 bits at
+// 28..31 (`decode_scalar`'s acc + (b << 28), internal.hpp:30-36).
+template <bool kDelta, bool kSwz, bool kF5 = false>
 __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w)[8], uint32_t T32, uint32_t sp,
-                                                uint32_t& carry) {
+                                                uint32_t& carry, uint32_t F5 = 0u) {
     const uint32_t tp = hibits4(~wp3);
     const uint32_t cm = pack28(wp3);
     // length of the integer ending at byte 0 = 4 - (last terminator among bytes -4..-1)
@@ -1164,6 +1178,22 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w
                     MVB_SLOT_DELTA("@p st.shared.u32 [%0], %1;\n\t");
 #undef MVB_SLOT_DELTA
             } else {
+#define MVB_SLOT_PLAIN5(STORE)                                                         \
+    asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b32 t, a;\n\t"                         \
+                 "and.b32 t, %2, %4;\n\t"                                                \
+                 "setp.ne.b32 p, t, 0;\n\t"                                              \
+                 "and.b32 a, %7, %4;\n\t"                                                \
+                 "setp.ne.b32 q, a, 0;\n\t"                                              \
+                 "shf.r.wrap.b32 t, %5, %6, %3;\n\t"                                     \
+                 "mul.hi.u32 t, t, %1;\n\t"                                              \
+                 "@q shf.r.wrap.b32 t, %5, %6, %8;\n\t" STORE                            \
+                 "@p add.u32 %0, %0, 4;\n\t"                                             \
+                 "mul.lo.u32 t, %1, 128;\n\t"                                            \
+                 "selp.b32 %1, 128, t, p;\n\t"                                           \
+                 "}"                                                                        \
+                 : "+r"(sp), "+r"(m)                                                        \
+                 : "r"(T32), "r"(fs), "r"(1u << e), "r"(lo), "r"(hi), "r"(F5), "r"(f5s)     \
+                 : "memory")
 #define MVB_SLOT_PLAIN(STORE)                                                          \
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"                           \
                  "and.b32 t, %2, %4;\n\t"                                                \
@@ -1177,12 +1207,20 @@ __device__ __forceinline__ void lane_slots_fast(uint32_t wp3, const uint32_t (&w
                  : "+r"(sp), "+r"(m)                                                        \
                  : "r"(T32), "r"(fs), "r"(1u << e), "r"(lo), "r"(hi)                        \
                  : "memory")
-                if (kSwz)
+                if (kF5) {
+                    const uint32_t f5s = 7 * t;
+                    if (kSwz)
+                        MVB_SLOT_PLAIN5("shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
+                                        "@p st.shared.u32 [a], t;\n\t");
+                    else
+                        MVB_SLOT_PLAIN5("@p st.shared.u32 [%0], t;\n\t");
+                } else if (kSwz)
                     MVB_SLOT_PLAIN("shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
                                    "@p st.shared.u32 [a], t;\n\t");
                 else
                     MVB_SLOT_PLAIN("@p st.shared.u32 [%0], t;\n\t");
 #undef MVB_SLOT_PLAIN
+#undef MVB_SLOT_PLAIN5
             }
         }
     }
@@ -1481,13 +1519,30 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
         const bool take2 = (inter || tail) && vote == 0;
         const bool takef = !take2 && (inter || (tail && !kDelta)) && !(vote & 2u);
+        // plain decode: 5-byte integers stay on the fast path (in slices dense
+        // enough for 32 slots to pay) when every byte
+        // after four continuation bytes (inside the range) is a terminator < 0x10
+        // (strict mode's check; longer runs then cannot occur either)
+        uint32_t F5 = 0u;
+        bool takef5 = false;
+        if (!kDelta && MVB_FAST5 && (vote & 2u) && (inter || tail) && n_w >= MVB_F5_MIN) {
+            uint32_t y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = w[k] | (w[k] << 1) | (w[k] << 2) | (w[k] << 3);
+            const uint32_t nz = hibits16(y[0], y[1], y[2], y[3]) | (hibits16(y[4], y[5], y[6], y[7]) << 16);
+            F5 = static_cast<uint32_t>(run4) & inr32;
+            takef5 = !__any_sync(0xFFFFFFFFu, (F5 & nz) != 0u);
+            F5 &= T32;
+        }
         if (n_w) last_i = i;
 #if MVB_PATH_STATS
-        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : takef ? 1 : inter ? 2 : 3], 1ull);
+        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : (takef || takef5) ? 1 : inter ? 2 : 3], 1ull);
 #endif
-        if (take2 || takef) {
+        if (take2 || takef || takef5) {
             if (take2)
                 lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+            else if (!kDelta && takef5)
+                lane_slots_fast<kDelta, kSwz, true>(wp3, w, T32, st_base + 4u * (a + wexcl), carry, F5);
             else
                 lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
             // the slice holds integer limit-1: record its end (stores past limit are

@@ -228,3 +228,57 @@ def test_two_byte_slices_dense_and_sparse_mix(oracle):
     ro, oo = oracle.decode_delta(enc, v.size, 5)
     rd, od = gpu_decode(enc, v.size, delta=True, prev=5)
     assert rd == ro and np.array_equal(od, oo)
+
+
+def _mixed5(rng, n):
+    """c1-like data: lengths uniform in 1..5, so nearly every slice holds
+    5-byte integers (the plain fast path's 5-byte slots)."""
+    return _values_of_lengths(rng, rng.integers(1, 6, n))
+
+
+@pytest.mark.parametrize("delta", [False, True])
+def test_mixed_five_byte_fifth_byte_checks(oracle, delta):
+    """Strict mode's fifth-byte rule inside otherwise canonical 1..5-byte
+    data: a 5-byte integer's fifth byte rewritten to 0x0F (largest valid),
+    0x10, 0x7F (malformed: the slice must leave the fast path) or a
+    continuation byte (a 6+-byte run), at lane / slice seams and mid-slice."""
+    rng = np.random.default_rng(515)
+    v = _mixed5(rng, 120_000)
+    enc = oracle.encode_sequence(v)
+    lens = 1 + sum((v >= (1 << s)).astype(np.int64) for s in (7, 14, 21, 28))
+    ends = np.cumsum(lens) - 1
+    fifth = ends[v >= (1 << 28)]  # byte index of each 5-byte integer's fifth byte
+    picks = []
+    for target in (31, 32, 33, 1023, 1024, 1025, 4096, 33_333, 70_001):
+        picks.append(int(fifth[np.searchsorted(fifth, target)]))
+    for pos in picks:
+        for val in (0x0F, 0x10, 0x7F, 0x80):
+            bad = enc.copy()
+            bad[pos] = val
+            if delta:
+                ro, oo = oracle.decode_delta(bad, v.size, 3)
+                r, out = gpu_decode(bad, v.size, delta=True, prev=3)
+            else:
+                ro, oo = oracle.decode(bad, v.size)
+                r, out = gpu_decode(bad, v.size)
+            assert r == ro and np.array_equal(out[: ro[1]], oo[: ro[1]]), (pos, val, delta)
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 33, 257, 1000, 4097, 100_003])
+def test_mixed_five_byte_ragged_sizes(oracle, n):
+    """1..5-byte data at ragged sizes through the device path (misaligned
+    input and output, guard words): tail slices of the plain fast path."""
+    import torch
+
+    rng = np.random.default_rng(9000 + n)
+    v = _mixed5(rng, n)
+    enc = oracle.encode_sequence(v)
+    for delta in (False, True):
+        ro, oo = oracle.decode_delta(enc, n, 17) if delta else oracle.decode(enc, n)
+        r, out = dev_decode(torch, torch.device("cuda", 0), enc, n, STRICT, delta, 17, 3, 1)
+        assert r == ro and np.array_equal(out, oo), (n, delta)
+        # and one integer short of the stream (count-1 in the last slice)
+        if n > 1:
+            ro, oo = oracle.decode_delta(enc, n - 1, 17) if delta else oracle.decode(enc, n - 1)
+            r, out = dev_decode(torch, torch.device("cuda", 0), enc, n - 1, STRICT, delta, 17, 0, 0)
+            assert r == ro and np.array_equal(out, oo), (n, delta)
