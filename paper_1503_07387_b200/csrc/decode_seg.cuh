@@ -164,6 +164,9 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
     return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
 }
 
+#ifndef MVB_A_PDL
+#define MVB_A_PDL 1  // kernel A launched as a programmatic dependent of the previous kernel B
+#endif
 #ifndef MVB_A_MINB
 #define MVB_A_MINB 1  // kernel A: minimum resident CTAs per SM (register cap)
 #endif
@@ -200,6 +203,11 @@ __global__ void __launch_bounds__(kSegThreads, MVB_A_MINB) vbyte_seg_totals(SegP
                           static_cast<uint32_t>((threadIdx.x >> 5) * kAStages * kSegASlice);
     if (it_begin < it_end) seg_totals_run<kDelta>(S, it_begin, it_end, lane, ring);
     (void)nw;
+#if MVB_A_PDL
+    // this grid completes only after the preceding grid did (kernel B of the
+    // previous decode, or anything else before it in the stream)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     // kernel B is launched as a programmatic dependent: it may start (and wait
     // in griddepcontrol.wait) once every CTA of this grid got here
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -303,6 +311,7 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
         }
         cp_async_commit();
     }
+    bool waited = false;  // griddepcontrol.wait done (MVB_A_PDL)
     uint32_t tcount = 0;  // terminators of the lane's bytes (inside the stream) in the current segment
     uint32_t sum = 0;     // digit-weight sum of the lane's bytes in the current segment
     long long s = it_begin / its_per_seg;
@@ -388,6 +397,15 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
             }
         }
         if (--to_flush == 0 || it + 1 == n_it) {  // leaving segment s: flush
+#if MVB_A_PDL
+            // launched as a programmatic dependent of the previous decode's kernel B:
+            // its last CTA re-zeroes these accumulators, so the first flush waits for
+            // it (the loads and digit sums above overlap its tail)
+            if (!waited) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
+#endif
             const unsigned c_tot = __reduce_add_sync(0xFFFFFFFFu, tcount);
             const uint32_t s_tot = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sum) : 0u;
             if (lane == 0) {
@@ -1941,6 +1959,11 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[0]));
 #endif
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#if MVB_A_PDL
+    // the next decode's kernel A may start its loads as this grid's CTAs retire
+    // (it waits for this grid before its first write)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 #if MVB_TRACE_B
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[1]));
 #endif

@@ -261,7 +261,25 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
         sl.grid_a_launch = static_cast<unsigned>(wa / mvbk::kSegWarps);
     }
     const unsigned grid_a = sl.grid_a_launch;
+#if MVB_A_PDL
+    {
+        // programmatic dependent of whatever precedes it: only a previous decode's
+        // kernel B triggers early, and A waits for it before its first write
+        cudaLaunchConfig_t ca = {};
+        ca.gridDim = dim3(grid_a);
+        ca.blockDim = dim3(mvbk::kSegThreads);
+        ca.dynamicSmemBytes = mvbk::kASmem;
+        ca.stream = s;
+        cudaLaunchAttribute aa[1];
+        aa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        aa[0].val.programmaticStreamSerializationAllowed = 1;
+        ca.attrs = aa;
+        ca.numAttrs = 1;
+        if (cudaLaunchKernelEx(&ca, mvbk::vbyte_seg_totals<Delta>, S) != cudaSuccess) return MVB_ERR_CUDA;
+    }
+#else
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
+#endif
     const unsigned grid_b = static_cast<unsigned>(ga < sl.grid_b_cap ? ga : sl.grid_b_cap);
     // programmatic dependent launch: B's CTAs launch as A's retire and wait for A's
     // results in griddepcontrol.wait (hides B's launch latency behind A's tail)
