@@ -164,6 +164,9 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
     return hb >= 31 ? 0u : (0x80808080u << (hb + 1)) & 0x80808080u;
 }
 
+#ifndef MVB_HEAD2
+#define MVB_HEAD2 1  // range head slices may take the 2-byte path
+#endif
 #ifndef MVB_A_PDL
 #define MVB_A_PDL 1  // kernel A launched as a programmatic dependent of the previous kernel B
 #endif
@@ -1535,7 +1538,10 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         const unsigned long long run2 = pair & 0xFFFFFFFFCull;              // a 3+-byte integer ends in 0..31
         const unsigned long long run4 = pair & (pair >> 2) & 0x1FFFFFFFFull;  // a 5+-byte integer ends in 0..31
         const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
-        const bool take2 = (inter || tail) && vote == 0;
+        // (a head slice -- bytes before the range start, read as 0x00 -- may take
+        // the 2-byte path too: its slots store at in-range terminators only, and
+        // the zero bytes add nothing to the candidates or the lane sums)
+        const bool take2 = (inter || tail || MVB_HEAD2) && vote == 0;
         const bool takef = !take2 && (inter || (tail && !kDelta)) && !(vote & 2u);
         // plain decode: 5-byte integers stay on the fast path (in slices dense
         // enough for 32 slots to pay) when every byte
@@ -1558,7 +1564,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
 #endif
         if (take2 || takef || takef5) {
             if (take2)
-                lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+                lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32 & inr32, st_base + 4u * (a + wexcl), carry);
             else if (!kDelta && takef5)
                 lane_slots_fast<kDelta, kSwz, true>(wp3, w, T32, st_base + 4u * (a + wexcl), carry, F5);
             else
@@ -1683,7 +1689,7 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             const uint32_t run2 = pair & 0xFFFFCu;     // a 3+-byte integer ends in 0..15
             const uint32_t run4 = pair & (pair >> 2);  // a 5+-byte integer ends in 0..15
             const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
-            const bool take2 = (inter || tail) && vote == 0;
+            const bool take2 = (inter || tail || MVB_HEAD2) && vote == 0;  // (head slices: see decode_range_ll)
             const bool takef = !take2 && inter && !(vote & 2u);
             if (n_w) last_i = i;
 #if MVB_PATH_STATS
@@ -1692,7 +1698,7 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             if (take2 || takef) {
                 if (take2) {
                     const uint32_t wv[4] = {w0, w1, w2, w3};
-                    lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16, st_base + 4u * (a + n_g + wexcl), carry);
+                    lane_slots_2b<kDelta, kSwz, 4>(wp3, wv, T16 & inr16, st_base + 4u * (a + n_g + wexcl), carry);
                 } else {
                     lane_slots_fast16<kDelta, kSwz>(wp3, w0, w1, w2, w3, T16, st_base + 4u * (a + n_g + wexcl), carry);
                 }

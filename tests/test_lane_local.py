@@ -282,3 +282,61 @@ def test_mixed_five_byte_ragged_sizes(oracle, n):
             ro, oo = oracle.decode_delta(enc, n - 1, 17) if delta else oracle.decode(enc, n - 1)
             r, out = dev_decode(torch, torch.device("cuda", 0), enc, n - 1, STRICT, delta, 17, 0, 0)
             assert r == ro and np.array_equal(out, oo), (n, delta)
+
+
+@pytest.mark.parametrize("delta", [False, True])
+def test_lists_head_slices_on_two_byte_path(oracle, delta):
+    """Lists of 1-2-byte integers starting at every offset inside a slice
+    (the head slice's bytes before the list read as zeros and must store
+    nothing), some count-limited inside the head slice, some with a 3-byte or
+    malformed integer in it (those heads leave the 2-byte path)."""
+    import torch
+
+    cuda = torch.device("cuda", 0)
+    rng = np.random.default_rng(4242)
+    parts, counts, reqs = [], [], []
+    for l in range(300):
+        n = int(rng.integers(1, 900))
+        lens = rng.integers(1, 3, n)
+        if l % 11 == 5:
+            lens[min(n - 1, int(rng.integers(0, 40)))] = 3
+        enc = oracle.encode_sequence(_values_of_lengths(rng, lens))
+        if l % 13 == 7 and enc.size > 12:
+            enc = enc.copy()
+            at = int(rng.integers(0, min(enc.size - 6, 60)))
+            enc[at:at + 6] = 0x80
+        gap = int(rng.integers(0, 64))  # junk bytes between lists: every start offset mod 16 / 512
+        parts.append(rng.integers(0, 256, gap).astype(np.uint8))
+        parts.append(enc)
+        counts.append(n)
+        reqs.append(n if l % 5 else max(1, int(rng.integers(1, min(n, 30) + 1))))
+    sizes = [p.size for p in parts]
+    starts = np.cumsum([0] + sizes)[1::2]  # byte offset of each list (after its junk gap)
+    data = np.concatenate(parts)
+    enc_sizes = np.array(sizes[1::2], np.int64)
+    # the batch alternates list l (entry 2l) and the junk gap after it (entry 2l+1,
+    # decoded too, ignored): byte_off[j] .. byte_off[j + 1] is entry j's bytes
+    byte_off = np.concatenate([[s, s + z] for s, z in zip(starts, enc_sizes)]).astype(np.uint64)
+    int_off = np.zeros(2 * len(counts), np.uint64)
+    acc = 0
+    for l, r in enumerate(reqs):
+        int_off[2 * l] = acc
+        int_off[2 * l + 1] = acc + r
+        acc += r + 3  # a gap in the output between lists
+    out = torch.full((acc + 4,), -1, dtype=torch.int32, device=cuda)
+    n_b = 2 * len(counts) - 1  # lists 2l are ours; odd entries decode the junk gaps, ignored
+    res = torch.zeros(n_b * 3, dtype=torch.int64, device=cuda)
+    prev = rng.integers(0, 1 << 32, n_b, dtype=np.uint64).astype(np.uint32)
+    d = mvb.Decoder(cuda, 1 << 16)
+    d.decode_lists(torch.from_numpy(data).to(cuda), torch.from_numpy(byte_off.view(np.int64)).to(cuda),
+                   torch.from_numpy(int_off.view(np.int64)).to(cuda), out,
+                   prev=torch.from_numpy(prev.view(np.int32)).to(cuda) if delta else None, results=res, delta=delta)
+    got = out.cpu().numpy().view(np.uint32)
+    rr = res.cpu().numpy().reshape(-1, 3)
+    for l in range(len(counts)):
+        span = data[int(byte_off[2 * l]):int(byte_off[2 * l + 1])]
+        r = reqs[l]
+        ro, oo = oracle.decode_delta(span, r, int(prev[2 * l])) if delta else oracle.decode(span, r)
+        assert tuple(int(x) for x in rr[2 * l]) == tuple(ro), l
+        n = ro[1]
+        assert np.array_equal(got[int(int_off[2 * l]):int(int_off[2 * l]) + n], oo[:n]), l
