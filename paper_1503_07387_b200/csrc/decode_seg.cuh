@@ -168,7 +168,7 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
 #define MVB_HEAD2 1  // range head slices may take the 2-byte path
 #endif
 #ifndef MVB_A_PDL
-#define MVB_A_PDL 1  // kernel A launched as a programmatic dependent of the previous kernel B
+#define MVB_A_PDL 1  // delta: kernel A launched as a programmatic dependent of the previous kernel B
 #endif
 #ifndef MVB_A_MINB
 #define MVB_A_MINB 1  // kernel A: minimum resident CTAs per SM (register cap)
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kSegThreads, MVB_A_MINB) vbyte_seg_totals(SegP
 #if MVB_A_PDL
     // this grid completes only after the preceding grid did (kernel B of the
     // previous decode, or anything else before it in the stream)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (kDelta) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
     // kernel B is launched as a programmatic dependent: it may start (and wait
     // in griddepcontrol.wait) once every CTA of this grid got here
@@ -401,10 +401,10 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
         }
         if (--to_flush == 0 || it + 1 == n_it) {  // leaving segment s: flush
 #if MVB_A_PDL
-            // launched as a programmatic dependent of the previous decode's kernel B:
-            // its last CTA re-zeroes these accumulators, so the first flush waits for
-            // it (the loads and digit sums above overlap its tail)
-            if (!waited) {
+            // (delta) launched as a programmatic dependent of the previous decode's
+            // kernel B: its last CTA re-zeroes these accumulators, so the first flush
+            // waits for it (the loads and digit sums above overlap its tail)
+            if (kDelta && !waited) {
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 waited = true;
             }

@@ -262,9 +262,10 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     }
     const unsigned grid_a = sl.grid_a_launch;
 #if MVB_A_PDL
-    {
+    if (Delta) {
         // programmatic dependent of whatever precedes it: only a previous decode's
         // kernel B triggers early, and A waits for it before its first write
+        // (delta only: plain decodes measured 2-4% slower with it)
         cudaLaunchConfig_t ca = {};
         ca.gridDim = dim3(grid_a);
         ca.blockDim = dim3(mvbk::kSegThreads);
@@ -276,6 +277,8 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
         ca.attrs = aa;
         ca.numAttrs = 1;
         if (cudaLaunchKernelEx(&ca, mvbk::vbyte_seg_totals<Delta>, S) != cudaSuccess) return MVB_ERR_CUDA;
+    } else {
+        mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
     }
 #else
     mvbk::vbyte_seg_totals<Delta><<<grid_a, mvbk::kSegThreads, mvbk::kASmem, s>>>(S);
