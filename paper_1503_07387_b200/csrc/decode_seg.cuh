@@ -760,7 +760,11 @@ constexpr int kLLSlice = 1024;                     // bytes per slice: 32 lanes 
 constexpr int kLaneGroup = 2;                      // (V/EP-sized staging: 2 x 512 integers)
 constexpr int kLaneStage = kLaneGroup * 512 + 32;  // staging words per warp (+ alignment), whole 128-byte rows
 constexpr int kLLWinBytes = 32 * 72;  // per warp: each lane's eight 8-byte digit windows (72-byte stride: 2 banks apart)
-constexpr int kLaneWarpBytes = 4 * kLaneStage + 3 * kLLSlice;  // staging (+ sparse windows) + 3-slice input ring
+#ifndef MVB_LL_NS
+#define MVB_LL_NS 3  // 32-byte-lane input ring: slices (MVB_LL_NS - 1 in flight ahead of the one decoded)
+#endif
+constexpr int kLLNS = MVB_LL_NS;
+constexpr int kLaneWarpBytes = 4 * kLaneStage + kLLNS * kLLSlice;  // staging (+ sparse windows) + input ring
 constexpr int kLaneSmem = kSegWarps * kLaneWarpBytes;
 static_assert((4 * kLaneStage) % 128 == 0 && kLaneWarpBytes % 128 == 0, "staging rows");
 
@@ -1472,7 +1476,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     }
     // input ring of kNS slices, kNS - 1 in flight ahead of the one decoded (one
     // commit group per slice, possibly empty)
-    constexpr int kNS = 3;
+    constexpr int kNS = kLLNS;
 #pragma unroll
     for (int j = 0; j < kNS - 1; ++j) {
         if (j >= i_lo && j < i_hi) {
