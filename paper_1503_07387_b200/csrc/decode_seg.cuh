@@ -171,7 +171,8 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
 #define MVB_A_PDL 1  // delta: kernel A launched as a programmatic dependent of the previous kernel B
 #endif
 #ifndef MVB_A_MINB
-#define MVB_A_MINB 1  // kernel A: minimum resident CTAs per SM (register cap)
+#define MVB_A_MINB 6  // kernel A: minimum resident CTAs per SM (80 registers, no spills; the delta
+                      // instantiation took 85 unbounded: 5 CTAs per SM, p50 delta +8%)
 #endif
 #ifndef MVB_A_CHUNKS
 #define MVB_A_CHUNKS 2
