@@ -180,7 +180,10 @@ __device__ __forceinline__ uint32_t after_last_terminator(uint32_t w) {
 constexpr int kSegAChunks = MVB_A_CHUNKS;          // kernel A: 16-byte chunks per lane per iteration
 constexpr int kSegASlice = 512 * kSegAChunks;      // bytes per warp iteration
 constexpr int kSegAW = 2 + 4 * kSegAChunks;        // words per lane: 2 halo + the lane's bytes
-constexpr int kAStages = 4;                        // kernel A: cp.async ring depth (iterations in flight)
+#ifndef MVB_A_STAGES
+#define MVB_A_STAGES 4
+#endif
+constexpr int kAStages = MVB_A_STAGES;             // kernel A: cp.async ring depth (iterations in flight; a power of 2)
 constexpr int kASmem = kSegWarps * kAStages * kSegASlice;
 
 // One warp walks a contiguous run of segments in kSegASlice-byte iterations

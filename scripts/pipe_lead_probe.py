@@ -1,6 +1,7 @@
 """Host drop-in (pipelined H2D / decode / D2H) time per call on a config at
-several first-chunk sizes; MVB_PIPE_LEAD (env, read once per process) sets how
-many chunks of input are queued ahead of the output."""
+several first-chunk sizes.  (It was written for an experimental MVB_PIPE_LEAD
+knob -- input chunks queued only a few chunks ahead of the output -- that made
+no difference and was removed; the env variable is now only echoed.)"""
 import ctypes, os, sys, time
 import numpy as np, torch
 sys.path.insert(0, ".")
