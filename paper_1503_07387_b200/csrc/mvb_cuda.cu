@@ -23,7 +23,7 @@
 #include "encode_kernel.cuh"
 
 #ifndef MVB_A_ITS
-#define MVB_A_ITS 8  // kernel A: at least this many 1 KiB iterations per warp
+#define MVB_A_ITS 6  // kernel A: at least this many 1 KiB iterations per warp (c2: one wave of 6 CTAs per SM)
 #endif
 
 namespace {
