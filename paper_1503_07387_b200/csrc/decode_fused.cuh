@@ -1,0 +1,735 @@
+// decode_fused.cuh -- the default strict-mode stream decoder: one persistent
+// kernel that reads the compressed stream from HBM exactly once.
+//
+// The stream (16-byte-aligned coordinates q = p + mis) is cut into units of
+// kUnit bytes.  Each warp owns a shared-memory buffer for one unit and takes
+// units u = 0, 1, 2, ... from a ticket counter:
+//
+//   load      one TMA bulk copy (cp.async.bulk + mbarrier) of the unit and the
+//             16 bytes before it into the warp's buffer (units at the stream's
+//             edges: masked loads);
+//   A(u)      the unit's terminator count and digit-weight sum, from shared
+//             memory (SegParams convention: the sums before a unit are the
+//             value sum of the integers before it plus the partial value of
+//             the integer straddling its start), published to a 32-ary tree of
+//             partial sums (level 0 = units, level l = blocks of 32^l units);
+//   prefix    the unit's output index and delta carry: the sums of at most 31
+//             published entries per level (one memory latency; the units
+//             before u took their tickets earlier, so their totals are out or
+//             about to be);
+//   B(u)      the lane-local decode (decode_range_ll's per-slice algorithm) of
+//             the unit's 1 KiB slices straight from the buffer, values staged
+//             per slice and copied out as 16-byte-aligned quads.
+//
+// Nothing but the tree's 16-byte entries and the output leaves the SM, and the
+// input crosses HBM once (the two-kernel decoder, decode_seg.cuh, read it
+// twice: its kernel B found the bytes in L2 only for streams up to ~100 MB).
+//
+// Tree entries are two 64-bit words, each carrying the launch's epoch as a
+// 24-bit tag next to its value (count << 24 | tag, sum << 32 | tag): a word
+// is written and read in one access, so a reader that sees this launch's tag
+// in both has the values -- no fences, and nothing is zeroed between
+// launches.  An entry is aggregated by the last of its children to arrive
+// (per-entry arrival counters only grow: every launch adds exactly the
+// entry's child count).  The last CTA to finish produces the DecodeResult
+// (fused_complete).  All CTAs must be co-resident (the grid is sized from the
+// occupancy calculator): a unit waits for the totals of every unit before it.
+//
+// Replaces the reference's stream loop (stream_loop.hpp:31-129) for
+// DecodeMode::strict with the semantics of decode_scalar / decode_delta_scalar
+// (vbyte.cpp:47-74, internal.hpp:22-37).
+#pragma once
+
+#include "decode_seg.cuh"
+
+namespace mvbk {
+
+#ifndef MVB_F_UNIT
+#define MVB_F_UNIT 4096  // bytes per unit (a multiple of 1 KiB)
+#endif
+#ifndef MVB_F_BLOCKS
+#define MVB_F_BLOCKS 4  // resident CTAs per SM (shared memory: one unit buffer + staging per warp)
+#endif
+constexpr int kFBlocks = MVB_F_BLOCKS;
+constexpr int kUnit = MVB_F_UNIT;
+constexpr int kUnitBuf = (16 + kUnit + 127) / 128 * 128;      // 16 halo bytes + the unit
+constexpr int kFWarpBytes = 2 * kUnitBuf + 4 * kLaneStage;    // two unit buffers + the slice staging
+constexpr int kFSmem = kSegWarps * kFWarpBytes + 16 * kSegWarps;  // + two mbarriers per warp
+constexpr int kFLevels = 6;                                   // tree levels: up to 32^6 units
+static_assert(kUnit % 1024 == 0 && kFWarpBytes % 128 == 0, "unit geometry");
+
+// One tree entry: (count << 24 | tag), (sum << 32 | tag); tag = epoch mod 2^24.
+struct alignas(16) FEntry {
+    unsigned long long c;
+    unsigned long long s;
+};
+
+struct FusedParams {
+    SegParams S;                 // in, mis, len, count, out, prev, prev_dev, seg_bytes (= kUnit), n_seg, hdr, res_dev
+    int swz;                     // staging swizzle: 0 never, 1 always, 2 dense units (debug switch)
+    int levels;                  // tree levels in use (32^levels >= n_seg)
+    long long n_at[kFLevels];    // entries per level (n_at[0] = n_seg)
+    FEntry* tree[kFLevels];      // level arrays
+    unsigned* arrive[kFLevels];  // per entry of levels >= 1: arrivals over all launches
+};
+
+// Digit-weight sum and continuation count of one word w (p = the word
+// before it), for streams whose integers have at most 3 bytes: a byte after
+// k continuation bytes weighs 128^k; classes 0/1 (weights 1 / 128) in one
+// dp4a, class 2 (2^14) in a second.  hi3 collects the bytes after three
+// continuation bytes (the caller then redoes the iteration exactly).
+__device__ __forceinline__ void ftot_word(uint32_t w, uint32_t p, uint32_t& cc, uint32_t& sA, uint32_t& sB,
+                                          uint32_t& hi3) {
+    const uint32_t ck = w & 0x80808080u, cp = p & 0x80808080u;
+    cc = __dp4a(ck, 0x01010101u, cc);                        // 128 per continuation byte
+    const uint32_t c1 = __funnelshift_l(cp, ck, 1);          // bit 0 of byte j: byte j-1 continues
+    const uint32_t c2 = c1 & __funnelshift_l(cp, ck, 9);     // ... and byte j-2
+    hi3 |= c2 & __funnelshift_l(cp, ck, 17);                 // ... and byte j-3
+    const uint32_t wa = c1 * 127u + 0x01010101u - c2 * 128u;  // 1, 128, or 0 (class 2)
+    const uint32_t w7 = w & 0x7F7F7F7Fu;
+    sA = __dp4a(w7, wa, sA);
+    sB = __dp4a(w7, c2, sB);
+}
+
+// The exact digit-weight sum of word w given the 8 bytes before it (p1 =
+// the word before, p2 = the one before that): weights 128^k for k = 0..4
+// continuation bytes before, 0 for five or more (2^35 = 0 mod 2^32).
+__device__ __forceinline__ uint32_t ftot_word_exact(uint32_t w, uint32_t p1, uint32_t p2) {
+    const uint32_t ck = w & 0x80808080u, c1p = p1 & 0x80808080u, c2p = p2 & 0x80808080u;
+    const uint32_t c1 = __funnelshift_l(c1p, ck, 1);
+    const uint32_t c2 = c1 & __funnelshift_l(c1p, ck, 9);
+    const uint32_t c3 = c2 & __funnelshift_l(c1p, ck, 17);
+    const uint32_t c4 = c3 & __funnelshift_l(c1p, ck, 25);
+    const uint32_t c5 = c4 & __funnelshift_l(c2p, c1p, 1);
+    const uint32_t w7 = w & 0x7F7F7F7Fu;
+    const uint32_t wa = c1 * 127u + 0x01010101u - c2 * 128u;  // classes 0, 1
+    const uint32_t wb = c2 + c3 * 127u - c4 * 128u;            // classes 2, 3 (x 2^14)
+    const uint32_t wc = c4 - c5;                                // class 4 (x 2^28)
+    return __dp4a(w7, wa, 0u) + (__dp4a(w7, wb, 0u) << 14) + (__dp4a(w7, wc, 0u) << 28);
+}
+
+// 16 bytes through the non-coherent path with an L2 evict-last policy (the
+// bytes are read again from L2 by the segment's decode, D units later)
+__device__ __forceinline__ uint4 ldg_keep16(const void* p, unsigned long long pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
+// Terminator count (inside the stream) and, for delta, digit-weight sum of
+// the segment bytes [q0, q1) (1 KiB iterations; lane l: bytes 32l .. 32l+31
+// of each).  Identical in every lane on return.
+template <bool kDelta>
+__device__ __forceinline__ void fused_totals(const SegParams& S, long long q0, long long q1, int lane,
+                                             unsigned& cnt_out, uint32_t& sum_out, uint32_t ubuf = 0u) {
+    const uint8_t* const ab = S.in - S.mis;
+    const long long qlo = S.mis, qhi = S.mis + S.len;
+    // ubuf: shared-memory address of byte q0 (the whole range and the 16 bytes
+    // before it are there, inside the stream), or 0: read global memory
+    uint32_t h1 = 0, h2 = 0;  // lane 0: the 8 bytes before the iteration (word -1, word -2)
+    if (lane == 0) {
+        if (ubuf) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(h2), "=r"(h1) : "r"(ubuf - 8u) : "memory");
+        } else {
+            h1 = seg_word(S, q0 - 4);
+            h2 = seg_word(S, q0 - 8);
+        }
+    }
+    unsigned tc = 0;      // terminators counted directly (edge iterations) + 32 per interior iteration
+    uint32_t cc = 0;      // 128 x continuation bytes of interior iterations
+    uint32_t sA = 0, sB = 0, sX = 0;
+    long long q = q0;
+    const unsigned long long pol = l2_evict_last();
+    uint4 x0, x1;
+    bool in0 = q >= qlo && q + 1024 <= qhi;
+    if (q < q1) {
+        const long long ql = q + 32 * lane;
+        if (ubuf) {
+            x0 = lds128(ubuf + static_cast<uint32_t>(ql - q0));
+            x1 = lds128(ubuf + static_cast<uint32_t>(ql - q0) + 16u);
+        } else if (in0) {
+            x0 = ldg_keep16(ab + ql, pol);
+            x1 = ldg_keep16(ab + ql + 16, pol);
+        } else {
+            x0 = seg_load16(S, ql);
+            x1 = seg_load16(S, ql + 16);
+        }
+    }
+    for (; q < q1; q += 1024) {
+        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        const bool inside = in0;
+        // prefetch the next iteration
+        const long long qn = q + 1024;
+        in0 = qn >= qlo && qn + 1024 <= qhi;
+        if (qn < q1) {
+            const long long ql = qn + 32 * lane;
+            if (ubuf) {
+                x0 = lds128(ubuf + static_cast<uint32_t>(ql - q0));
+                x1 = lds128(ubuf + static_cast<uint32_t>(ql - q0) + 16u);
+            } else if (in0) {
+                x0 = ldg_keep16(ab + ql, pol);
+                x1 = ldg_keep16(ab + ql + 16, pol);
+            } else {
+                x0 = seg_load16(S, ql);
+                x1 = seg_load16(S, ql + 16);
+            }
+        }
+        uint32_t p1 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1), p2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
+        const uint32_t l1 = __shfl_sync(0xFFFFFFFFu, w[7], 31), l2 = __shfl_sync(0xFFFFFFFFu, w[6], 31);
+        if (lane == 0) {
+            p1 = h1;
+            p2 = h2;
+        }
+        h1 = l1;
+        h2 = l2;
+        if (inside) {
+            tc += 32;
+        } else {
+            const long long ql = q + 32 * lane;
+            tc += __popc(hibits16(~w[0], ~w[1], ~w[2], ~w[3]) & seg_inr16(S, ql)) +
+                  __popc(hibits16(~w[4], ~w[5], ~w[6], ~w[7]) & seg_inr16(S, ql + 16));
+        }
+        if (kDelta) {
+            uint32_t hi3 = 0, a = 0, b = 0, ccx = 0;
+            ftot_word(w[0], p1, ccx, a, b, hi3);
+#pragma unroll
+            for (int k = 1; k < 8; ++k) ftot_word(w[k], w[k - 1], ccx, a, b, hi3);
+            if (__any_sync(0xFFFFFFFFu, hi3 != 0)) {  // an integer of 4+ bytes: the exact weights
+                uint32_t s = ftot_word_exact(w[0], p1, p2) + ftot_word_exact(w[1], w[0], p1);
+#pragma unroll
+                for (int k = 2; k < 8; ++k) s += ftot_word_exact(w[k], w[k - 1], w[k - 2]);
+                sX += s;
+            } else {
+                sA += a;
+                sB += b;
+            }
+            if (inside) cc += ccx;
+        } else if (inside) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cc = __dp4a(w[k] & 0x80808080u, 0x01010101u, cc);
+        }
+    }
+    unsigned cnt = tc - (cc >> 7);
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    uint32_t sum = 0;
+    if (kDelta) sum = __reduce_add_sync(0xFFFFFFFFu, sA + (sB << 14) + sX);
+    cnt_out = cnt;
+    sum_out = sum;
+}
+
+// ---- delta slices whose integers have at most 3 bytes (c2, c4: nearly every slice) ----
+//
+// Every byte b contributes d(b) * 128^k to the running sum, k = the number of
+// continuation bytes right before it (0..2 here), so the delta output at
+// terminator t is carry + (the sum of all contributions up to t): one dp2a
+// per byte (two 16-bit weights x two digit bytes, plus an accumulator),
+// with the previous output as the accumulator.  No integer value is ever
+// assembled.  The carry of this path counts every byte before the slice
+// (including the partial integer straddling into it); the other paths count
+// complete integers only, so the carry is converted at entry and exit.
+
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// The partial value of the bytes of word x after its last terminator (all
+// four if it has none): the part of an integer that continues past x.
+__device__ __forceinline__ uint32_t tail_value(uint32_t x) {
+    return shr_clamp(pack28(x), 7 * (32 - __clz(static_cast<int>(hibits4(~x)))));
+}
+
+// One predicated staging store: if bit `bit` of T is set, stage[sp] = v, sp += 4.
+template <bool kSwz>
+__device__ __forceinline__ void slot_store(uint32_t& sp, uint32_t T, uint32_t bit, uint32_t v) {
+    if (kSwz)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"
+            "and.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t"
+            "shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
+            "@p st.shared.u32 [a], %3;\n\t@p add.u32 %0, %0, 4;\n\t}"
+            : "+r"(sp)
+            : "r"(T), "r"(bit), "r"(v)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t"
+            "@p st.shared.u32 [%0], %3;\n\t@p add.u32 %0, %0, 4;\n\t}"
+            : "+r"(sp)
+            : "r"(T), "r"(bit), "r"(v)
+            : "memory");
+}
+
+// wp3: the 4 bytes before the lane; w: its 32 bytes; T: its in-range
+// terminators (bit j = byte j); sp: staging address of its first output;
+// carry (in/out, warp-uniform): the byte-convention carry before the slice.
+template <bool kSwz>
+__device__ __forceinline__ void lane_slots_d3(uint32_t wp3, const uint32_t (&w)[8], uint32_t T, uint32_t sp,
+                                              uint32_t& carry) {
+    uint32_t W01[8], W23[8], w7[8];
+    uint32_t tot = 0, prev = wp3;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t s8 = __funnelshift_l(prev, w[k], 8), s16 = __funnelshift_l(prev, w[k], 16);
+        // byte j: 1 if byte j-1 continues, 0x81 if bytes j-1 and j-2 do
+        const uint32_t x = ((s8 >> 7) & 0x01010101u) | (s8 & s16 & 0x80808080u);
+        // 16-bit weights 1 + 127 x: 1, 128, 16384
+        W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
+        W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
+        w7[k] = w[k] & 0x7F7F7F7Fu;
+        tot = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], tot));
+        prev = w[k];
+    }
+    uint32_t acc = lane_scan_offset<true>(tot, carry);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
+        const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
+        const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
+        acc = dp2a_hi(W23[k], w7[k], o1);
+        slot_store<kSwz>(sp, T, 1u << (4 * k), o0);
+        slot_store<kSwz>(sp, T, 2u << (4 * k), o1);
+        slot_store<kSwz>(sp, T, 4u << (4 * k), o2);
+        slot_store<kSwz>(sp, T, 8u << (4 * k), acc);
+    }
+}
+
+// decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
+// shared memory at ubuf (byte qs; the 16 bytes before it too), or -- ubuf 0,
+// units at the stream's edges -- read from global memory with range masks.
+template <bool kDelta, bool kSwz>
+__device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs, long long qe,
+                                                unsigned long long base, uint32_t carry, unsigned long long limit,
+                                                uint32_t* out, uint32_t* stage, uint32_t ubuf, int lane,
+                                                const RangeSink& K, RangeOut& ro) {
+    const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
+    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const int ns = static_cast<int>((qe - qs + kLLSlice - 1) / kLLSlice);
+    int i_lo, i_hi;  // interior slices: i_lo <= i < i_hi
+    {
+        const long long d = R.lo - qs, e = R.hi - qs;
+        const long long lo = d <= 0 ? 0 : (d + kLLSlice - 1) / kLLSlice;
+        const long long hi = e <= 0 ? 0 : e / kLLSlice;
+        i_lo = static_cast<int>(lo < ns ? lo : ns);
+        i_hi = static_cast<int>(hi < ns ? hi : ns);
+    }
+    unsigned long long run = base;  // output index of the slice's first integer
+    int last_i = -1;                // the last slice holding an integer (warp-uniform)
+    uint32_t pw2 = 0, pw3 = 0;      // lane 0: the 8 bytes before the slice
+    if (lane == 0) {
+        if (ubuf) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(pw2), "=r"(pw3) : "r"(ubuf - 8u) : "memory");
+        } else if (r_inside(R, qs - 8, 8)) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(R.ab + qs - 8));
+            pw2 = v.x;
+            pw3 = v.y;
+        } else {
+            pw2 = r_word(R, qs - 8);
+            pw3 = r_word(R, qs - 4);
+        }
+    }
+#pragma unroll 1
+    for (int i = 0; i < ns; ++i) {
+        const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
+        const bool inter = i >= i_lo && i < i_hi;                      // warp-uniform
+        const long long q0 = qs + static_cast<long long>(kLLSlice) * i + 32 * lane;
+        uint4 x0, x1;
+        if (inter && ubuf) {
+            const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * i + 32 * lane);
+            x0 = lds128(sa);
+            x1 = lds128(sa + 16u);
+        } else {
+            x0 = r_load16(R, q0);
+            x1 = r_load16(R, q0 + 16);
+        }
+        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1), wp2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
+        const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31), l2 = __shfl_sync(0xFFFFFFFFu, w[6], 31);
+        if (lane == 0) {
+            wp3 = pw3;
+            wp2 = pw2;
+        }
+        pw3 = l3;
+        pw2 = l2;
+        const uint32_t T32 = hibits16(~w[0], ~w[1], ~w[2], ~w[3]) | (hibits16(~w[4], ~w[5], ~w[6], ~w[7]) << 16);
+        const uint32_t inr32 = inter ? 0xFFFFFFFFu : (r_inr16(R, q0) | (r_inr16(R, q0 + 16) << 16));
+        const uint32_t n_own = __popc(T32 & inr32);
+        uint32_t incl = n_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t wexcl = incl - n_own;
+        // four continuation bytes in a row anywhere in positions -4..31
+        // a tail slice (bytes past the range end only, read as 0x80: never
+        // terminators) may take the fast paths too (delta: the 2-byte one only --
+        // the fast path's lane sum assumes a terminator in the lane's last word);
+        // its vote counts continuation bytes inside the range only
+        const bool tail = !inter && qs + static_cast<long long>(kLLSlice) * i >= R.lo;
+        const unsigned long long C = (static_cast<unsigned long long>(~T32 & inr32) << 4) |
+                                     (~hibits4(~wp3) & (inter ? 0xFu : halo_in_range(R, q0)));
+        const unsigned long long pair = C & (C >> 1);                       // bit j: positions j-4, j-3 continue
+        const unsigned long long run2 = pair & 0xFFFFFFFFCull;              // a 3+-byte integer ends in 0..31
+        const unsigned long long run4 = pair & (pair >> 2) & 0x1FFFFFFFFull;  // a 5+-byte integer ends in 0..31
+        const unsigned vote = (__any_sync(0xFFFFFFFFu, run2 != 0) ? 1u : 0u) | (__any_sync(0xFFFFFFFFu, run4 != 0) ? 2u : 0u);
+        // (a head slice -- bytes before the range start, read as 0x00 -- may take
+        // the 2-byte path too: its slots store at in-range terminators only, and
+        // the zero bytes add nothing to the candidates or the lane sums)
+        // delta: no byte after three continuation bytes in positions 0..31 (every
+        // integer ending here has at most 3 bytes) -> the dp2a path
+        bool take3 = false;
+        if (kDelta) {
+            const unsigned long long t3 = C & (C >> 1) & (C >> 2) & 0x1FFFFFFFEull;
+            take3 = (inter || tail || MVB_HEAD2) && !__any_sync(0xFFFFFFFFu, t3 != 0);
+        }
+        const bool take2 = (inter || tail || MVB_HEAD2) && vote == 0;
+        const bool takef = !take2 && (inter || (tail && !kDelta)) && !(vote & 2u);
+        // plain decode: 5-byte integers stay on the fast path (in slices dense
+        // enough for 32 slots to pay) when every byte
+        // after four continuation bytes (inside the range) is a terminator < 0x10
+        // (strict mode's check; longer runs then cannot occur either)
+        uint32_t F5 = 0u;
+        bool takef5 = false;
+        if (!kDelta && MVB_FAST5 && (vote & 2u) && (inter || tail) && n_w >= MVB_F5_MIN) {
+            uint32_t y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = w[k] | (w[k] << 1) | (w[k] << 2) | (w[k] << 3);
+            const uint32_t nz = hibits16(y[0], y[1], y[2], y[3]) | (hibits16(y[4], y[5], y[6], y[7]) << 16);
+            F5 = static_cast<uint32_t>(run4) & inr32;
+            takef5 = !__any_sync(0xFFFFFFFFu, (F5 & nz) != 0u);
+            F5 &= T32;
+        }
+        if (n_w) last_i = i;
+#if MVB_PATH_STATS
+        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : (takef || takef5) ? 1 : inter ? 2 : 3], 1ull);
+#endif
+        if (take3) {
+            // carry: complete integers before the slice -> every byte before it
+            const uint32_t hin = __shfl_sync(0xFFFFFFFFu, tail_value(wp3), 0);
+            const uint32_t hout = __shfl_sync(0xFFFFFFFFu, tail_value(w[7]), 31);
+            carry += hin;
+            lane_slots_d3<kSwz>(wp3, w, T32 & inr32, st_base + 4u * (a + wexcl), carry);
+            carry -= hout;
+            if (run < limit && run + n_w >= limit)
+                slice_count_end(R, K, q0, T32 & inr32, static_cast<uint32_t>(limit - 1 - run), wexcl, n_own);
+        } else if (take2 || takef || takef5) {
+            if (take2)
+                lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32 & inr32, st_base + 4u * (a + wexcl), carry);
+            else if (!kDelta && takef5)
+                lane_slots_fast<kDelta, kSwz, true>(wp3, w, T32, st_base + 4u * (a + wexcl), carry, F5);
+            else
+                lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
+            // the slice holds integer limit-1: record its end (stores past limit are
+            // dropped by the copy-out)
+            if (run < limit && run + n_w >= limit)
+                slice_count_end(R, K, q0, T32 & inr32, static_cast<uint32_t>(limit - 1 - run), wexcl, n_own);
+        } else
+            carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
+                                               st_base + 4u * (a + wexcl), st_base + kSparseWin + 72u * lane, carry);
+        if (n_w == 0) continue;
+        __syncwarp();
+        stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
+        run += n_w;
+        __syncwarp();  // the staging buffer is rewritten by the next slice
+    }
+    // the end of the range's last integer: in slice last_i
+    long long last_end = -1;
+    if (last_i >= 0 && !K.hdr) {  // (a stream decode finds the stream's last integer in its completion)
+        const long long q0 = qs + static_cast<long long>(kLLSlice) * last_i + 32 * lane;
+        const uint4 x0 = r_load16(R, q0), x1 = r_load16(R, q0 + 16);
+        const uint32_t e0 = hibits16(~x0.x, ~x0.y, ~x0.z, ~x0.w) & r_inr16(R, q0);
+        const uint32_t e1 = hibits16(~x1.x, ~x1.y, ~x1.z, ~x1.w) & r_inr16(R, q0 + 16);
+        if (e1) last_end = q0 + 16 + (31 - __clz(e1)) + 1 - R.lo;
+        else if (e0) last_end = q0 + (31 - __clz(e0)) + 1 - R.lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long le = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
+            last_end = le > last_end ? le : last_end;
+        }
+    }
+    ro.last_end = last_end;
+    ro.n = run - base;
+}
+
+__device__ __forceinline__ void fentry_put(FEntry* e, unsigned long long cnt, uint32_t sum, unsigned tag) {
+    const ulonglong2 v = make_ulonglong2((cnt << 24) | tag, (static_cast<unsigned long long>(sum) << 32) | tag);
+    asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(e), "l"(v.x), "l"(v.y) : "memory");
+}
+// Wait for entry e of this launch (tag) and return its count and sum.
+__device__ __forceinline__ void fentry_get(const FEntry* e, unsigned tag, unsigned long long& cnt, uint32_t& sum) {
+    unsigned long long c, s;
+    for (;;) {
+        asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(s) : "l"(e) : "memory");
+        if ((c & 0xFFFFFFull) == tag && (s & 0xFFFFFFull) == tag) break;
+        __nanosleep(32);
+    }
+    cnt = c >> 24;
+    sum = static_cast<uint32_t>(s >> 32);
+}
+
+// Publish entry i of level l (one lane) and aggregate upwards: the last
+// child to arrive at a parent sums the parent's children (the whole warp).
+__device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long long i, unsigned long long cnt,
+                                              uint32_t sum, unsigned tag, int lane) {
+    for (;;) {
+        if (lane == 0) fentry_put(F.tree[l] + i, cnt, sum, tag);
+        if (l + 1 >= F.levels) return;
+        const long long par = i >> 5;
+        const unsigned kids = static_cast<unsigned>((F.n_at[l] - (par << 5)) < 32 ? F.n_at[l] - (par << 5) : 32);
+        unsigned last = 0;
+        if (lane == 0) last = (atomicAdd(F.arrive[l + 1] + par, 1u) + 1u) % kids == 0u ? 1u : 0u;
+        last = __shfl_sync(0xFFFFFFFFu, last, 0);
+        if (!last) return;
+        unsigned long long c = 0;
+        uint32_t s = 0;
+        if (lane < kids) fentry_get(F.tree[l] + (par << 5) + lane, tag, c, s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        }
+        cnt = c;
+        sum = s;
+        i = par;
+        ++l;
+    }
+}
+
+// Sum of the entries before index v at every level (all lanes get it): the
+// count and value sum of segments [0, v).  Waits for entries not yet
+// published in this launch.
+__device__ __forceinline__ void fused_prefix(const FusedParams& F, long long v, unsigned tag, int lane,
+                                             unsigned long long& cnt, unsigned long long& sum) {
+    unsigned long long c = 0, s = 0;
+    for (int l = 0; l < F.levels; ++l) {
+        const long long d = (v >> (5 * l)) & 31;
+        if (lane < d) {
+            unsigned long long ec;
+            uint32_t es;
+            fentry_get(F.tree[l] + (((v >> (5 * l)) >> 5) << 5) + lane, tag, ec, es);
+            c += ec;
+            s += es;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    }
+    cnt = c;
+    sum = s;
+}
+
+// Completion (all threads of every CTA): the last CTA produces the DecodeResult.
+__device__ __forceinline__ void fused_complete(const FusedParams& F, unsigned tag) {
+    const SegParams& S = F.S;
+    __shared__ bool s_last;
+    __shared__ long long s_seg;
+    __shared__ unsigned long long s_total;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&S.hdr->done, 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < 32) {
+        unsigned long long c, u;
+        fused_prefix(F, S.n_seg, tag, threadIdx.x, c, u);
+        if (threadIdx.x == 0) s_total = c;
+    }
+    __syncthreads();
+    const unsigned long long total = s_total;
+    WsHeader* h = S.hdr;
+    const unsigned long long err_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_idx_inv);
+    const bool truncated = !(err_inv != 0ull && ~err_inv < S.count) && total < S.count;  // (CTA-uniform)
+    long long last_end_found = 0;
+    if (truncated) {
+        // the end of the stream's last integer: the last segment holding one,
+        // then its last terminator byte
+        if (threadIdx.x == 0) s_seg = -1;
+        __syncthreads();
+        for (long long hi = S.n_seg - 1; hi >= 0; hi -= blockDim.x) {
+            const long long k = hi - static_cast<long long>(threadIdx.x);
+            if (k >= 0 && (__ldcg(&F.tree[0][k].c) >> 24) > 0) atomicMax(&s_seg, k);
+            __syncthreads();
+            if (s_seg >= 0) break;
+        }
+        if (s_seg >= 0) {
+            __shared__ long long s_le;
+            const long long p_lo = s_seg * S.seg_bytes - S.mis > 0 ? s_seg * S.seg_bytes - S.mis : 0;
+            long long p_hi = (s_seg + 1) * S.seg_bytes - S.mis;
+            if (p_hi > S.len) p_hi = S.len;
+            for (long long top = p_hi; top > p_lo; top -= 16ll * blockDim.x) {
+                if (threadIdx.x == 0) s_le = -1;
+                __syncthreads();
+                const long long b = top - 16ll * (threadIdx.x + 1);
+                long long le = -1;
+                for (int j = 15; j >= 0 && le < 0; --j) {
+                    const long long p = b + j;
+                    if (p >= p_lo && p < p_hi && S.in[p] < 0x80u) le = p + 1;
+                }
+                if (le >= 0) atomicMax(&s_le, le);
+                __syncthreads();
+                if (s_le >= 0) break;
+            }
+            if (threadIdx.x == 0) last_end_found = s_le > 0 ? s_le : 0;
+        }
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long errpos_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_pos_inv);
+        const unsigned long long count_end = *reinterpret_cast<volatile unsigned long long*>(&h->count_end);
+        mvb_result r;
+        r.reserved = 0;
+        if (err_inv != 0ull && ~err_inv < S.count) {
+            r.status = MVB_MALFORMED;
+            r.values_written = ~err_inv;
+            r.bytes_consumed = ~errpos_inv;
+        } else if (total >= S.count) {
+            r.status = MVB_OK;
+            r.values_written = S.count;
+            r.bytes_consumed = count_end;
+        } else {
+            r.status = MVB_TRUNCATED;
+            r.values_written = total;
+            r.bytes_consumed = static_cast<unsigned long long>(last_end_found);
+        }
+        h->result = r;
+        if (S.res_dev) *S.res_dev = r;
+        h->done = 0;
+        h->ticket = 0;
+        h->err_idx_inv = 0;
+        h->err_pos_inv = 0;
+        h->last_end = 0;
+        h->count_end = 0;
+        h->epoch = h->epoch + 1;
+    }
+    __threadfence();
+}
+
+__device__ __forceinline__ void mbar_init_warp(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// One TMA bulk copy of `bytes` (multiple of 16, 16-byte-aligned ends) into
+// shared memory, completing on the mbarrier (issued by one lane).
+__device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst come first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(const __grid_constant__ FusedParams F) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const SegParams& S = F.S;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint8_t* const wbuf = smem + wid * kFWarpBytes;  // two unit buffers: [0, 16) the bytes before, then the unit
+    uint32_t* const stage = reinterpret_cast<uint32_t*>(wbuf + 2 * kUnitBuf);
+    unsigned long long* const bar_p = reinterpret_cast<unsigned long long*>(smem + kSegWarps * kFWarpBytes) + 2 * wid;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(bar_p));
+    const uint32_t buf0 = static_cast<uint32_t>(__cvta_generic_to_shared(wbuf));
+    if (lane == 0) {
+        mbar_init_warp(bar_p);
+        mbar_init_warp(bar_p + 1);
+    }
+    __syncwarp();
+    uint32_t phases = 0;  // bit b: parity of buffer b's next completion
+    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
+    const long long q_stream_end = (R.hi + 15) & ~15ll;
+    const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
+    // the previous grid on the stream (e.g. the previous decode on this
+    // workspace: it resets the ticket and advances the epoch) is complete and
+    // visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const unsigned tag =
+        static_cast<unsigned>(*reinterpret_cast<volatile unsigned long long*>(&S.hdr->epoch) + 1ull) & 0xFFFFFFu;
+    const uint32_t prev0 = kDelta ? (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
+    // Pipeline per warp: take unit u, load it, total it and publish -- then
+    // decode the unit taken one iteration earlier (its predecessors took their
+    // tickets before it and published right after, so its prefix is out).
+    long long up = -1;  // the unit awaiting its decode (buffer bp)
+    int bp = 0;
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
+        const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+        // output index and carry of unit up (loads overlap the ticket's)
+        unsigned long long base = 0, csum = 0;
+        if (up >= 0) fused_prefix(F, up, tag, lane, base, csum);
+        if (u < S.n_seg) {
+            const int b = bp ^ 1;
+            const long long qs = u * kUnit;
+            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
+            const uint32_t ubuf = staged ? buf0 + b * kUnitBuf + 16u : 0u;
+            if (staged) {
+                if (lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qs - 16, kUnit + 16, bar0 + 8u * b);
+                while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
+                }
+                phases ^= 1u << b;
+            }
+            unsigned c;
+            uint32_t su;
+            fused_totals<kDelta>(S, qs, qs + kUnit, lane, c, su, ubuf);
+            fused_publish(F, 0, u, c, su, tag, lane);
+        }
+        if (up >= 0 && base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
+            const long long qs = up * kUnit;
+            const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
+            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;
+            const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
+            uint32_t straddle = 0;
+            if (kDelta) {
+                uint32_t wb;
+                if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
+                else wb = r_word(R, qs - 4);
+                straddle = shr_clamp(pack28(wb), 7 * (32 - __clz(static_cast<int>(hibits4(~wb)))));
+            }
+            const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
+            bool swz = F.swz == 1;
+            if (F.swz == 2) {
+                unsigned long long n_own;
+                uint32_t unused;
+                fentry_get(F.tree[0] + up, tag, n_own, unused);
+                swz = range_dense(n_own, qe - qs);
+            }
+            RangeOut ro;
+            if (swz)
+                decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
+            else
+                decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
+            __syncwarp();  // (buffer bp is refilled next iteration)
+        }
+        if (u >= S.n_seg) break;
+        up = u;
+        bp ^= 1;
+    }
+    fused_complete(F, tag);
+}
+
+}  // namespace mvbk

@@ -118,6 +118,22 @@ __device__ __forceinline__ uint32_t seg_inr16(const SegParams& S, long long q0) 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+// L2 eviction-priority policies (createpolicy) for cache-hinted accesses
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// cp.async whose L2 line may go first (the decode's last read of the input)
+__device__ __forceinline__ void cp_async16_ef(uint32_t dst, const void* src, unsigned long long pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1423,23 +1439,32 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
         if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {
             uint32_t v;
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(stg_addr<kSwz>(st_base + 4u * i)) : "memory");
-            ob[i] = v;
+            __stcs(ob + i, v);
         }
     }
-    // whole quads: a shared address and a global pointer that both advance by
-    // one warp-row per iteration (no per-store 64-bit index arithmetic)
+    // whole quads: lane l copies quads q = i0/4 + l + 32m.  Swizzled, quad q
+    // sits at q ^ ((q >> 3) & 7), and (q >> 3) & 7 only flips bit 2 from one m
+    // to the next, so even and odd m each keep one base address advancing by
+    // 1 KiB; four quads per iteration with immediate offsets.
+    // (the swizzle is a function of the absolute shared-memory address: quad
+    // index Q = address / 16)
     uint32_t i = i0 + 4 * lane;
-    uint32_t sa = st_base + 4u * i;
+    const uint32_t Q = (st_base >> 4) + (i >> 2);
+    const uint32_t Qs = kSwz ? (Q ^ ((Q >> 3) & 7u)) : Q;
+    const uint32_t ae = 16u * Qs, ao = kSwz ? 16u * (Qs ^ 4u) : 16u * Qs;
     uint4* dst = reinterpret_cast<uint4*>(ob + i);
-#pragma unroll 4
-    for (; i < i1; i += 128, sa += 512u, dst += 32) {
-        uint4 v;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "r"(stg_addr<kSwz>(sa))
-                     : "memory");
-        *dst = v;
+    uint32_t off = 0;  // shared-memory bytes advanced (both bases)
+    for (; i + 384 < i1; i += 512, off += 2048u, dst += 128) {
+        const uint4 v0 = lds128(ae + off), v1 = lds128(ao + off + 512u);
+        const uint4 v2 = lds128(ae + off + 1024u), v3 = lds128(ao + off + 1536u);
+        __stcs(dst, v0);
+        __stcs(dst + 32, v1);
+        __stcs(dst + 64, v2);
+        __stcs(dst + 96, v3);
     }
+    if (i < i1) __stcs(dst, lds128(ae + off));
+    if (i + 128 < i1) __stcs(dst + 32, lds128(ao + off + 512u));
+    if (i + 256 < i1) __stcs(dst + 64, lds128(ae + off + 1024u));
 }
 
 
@@ -1481,11 +1506,12 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     // input ring of kNS slices, kNS - 1 in flight ahead of the one decoded (one
     // commit group per slice, possibly empty)
     constexpr int kNS = kLLNS;
+    const unsigned long long pol = l2_evict_first();
 #pragma unroll
     for (int j = 0; j < kNS - 1; ++j) {
         if (j >= i_lo && j < i_hi) {
-            cp_async16(rbase + kLLSlice * j, pin + kLLSlice * j);
-            cp_async16(rbase + kLLSlice * j + 16, pin + kLLSlice * j + 16);
+            cp_async16_ef(rbase + kLLSlice * j, pin + kLLSlice * j, pol);
+            cp_async16_ef(rbase + kLLSlice * j + 16, pin + kLLSlice * j + 16, pol);
         }
         cp_async_commit();
     }
@@ -1497,8 +1523,8 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
         {
             const int j = i + kNS - 1;
             if (j >= i_lo && j < i_hi) {
-                cp_async16(rbase + o_wr, pin + static_cast<long long>(kLLSlice) * j);
-                cp_async16(rbase + o_wr + 16, pin + static_cast<long long>(kLLSlice) * j + 16);
+                cp_async16_ef(rbase + o_wr, pin + static_cast<long long>(kLLSlice) * j, pol);
+                cp_async16_ef(rbase + o_wr + 16, pin + static_cast<long long>(kLLSlice) * j + 16, pol);
             }
             cp_async_commit();
             o_wr = o_wr + kLLSlice == kLLSlice * kNS ? 0u : o_wr + kLLSlice;

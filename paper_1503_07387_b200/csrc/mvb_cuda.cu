@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -18,6 +19,7 @@
 #include "decode_pipelined.cuh"
 #include "decode_v3.cuh"
 #include "decode_seg.cuh"
+#include "decode_fused.cuh"
 #include "decode_warp.cuh"
 #include "totals_kernel.cuh"
 #include "encode_kernel.cuh"
@@ -308,6 +310,115 @@ int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     return seg_launch_pair<Delta, LL>(sl, 0, sl.S.n_seg, true, nullptr, nullptr, nullptr, s);
 }
 
+// Occupancy of a kernel on the current device (cached per kernel and device).
+int occupancy(const void* fn, int threads, size_t smem, int* sms_out) {
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    *sms_out = sms;
+    const unsigned long long key = (reinterpret_cast<uintptr_t>(fn) << 8) ^ static_cast<unsigned long long>(dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return -1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return -1;
+    if (n < 1) n = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = n;
+    return n;
+}
+
+// Single-read strict decode (decode_fused.cuh): one persistent launch over
+// units of mvbk::kUnit bytes.
+int g_fused_swz = [] {
+    const char* e = std::getenv("MVB_F_SWZ");  // (debug runs)
+    return e ? std::atoi(e) : 2;
+}();
+
+struct FusedPlan {
+    long long n_seg, W;
+    int levels;
+    long long n_at[mvbk::kFLevels];
+    size_t need;
+};
+
+FusedPlan fused_plan(long long qlen, long long W_max) {
+    FusedPlan f = {};
+    f.n_seg = (qlen + mvbk::kUnit - 1) / mvbk::kUnit;
+    f.W = std::min<long long>(W_max, (f.n_seg + mvbk::kSegWarps - 1) / mvbk::kSegWarps * mvbk::kSegWarps);
+    f.levels = 1;
+    long long span = 32;
+    while (span <= f.n_seg && f.levels < mvbk::kFLevels) {
+        span *= 32;
+        ++f.levels;
+    }
+    f.need = kHeaderBytes;
+    long long n = f.n_seg;
+    for (int l = 0; l < f.levels; ++l) {
+        f.n_at[l] = n;
+        f.need += sizeof(mvbk::FEntry) * static_cast<size_t>(n) + (l ? 4 * static_cast<size_t>(n) : 0);
+        f.need = (f.need + 15) / 16 * 16;
+        n = (n + 31) / 32;
+    }
+    return f;
+}
+
+template <bool Delta>
+int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+    int sms = 0;
+    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta>), mvbk::kSegThreads,
+                                 mvbk::kFSmem, &sms);
+    if (per_sm < 0) return MVB_ERR_CUDA;
+    const long long W_max = static_cast<long long>(per_sm) * sms * mvbk::kSegWarps;
+    const FusedPlan f = fused_plan(p.mis + p.len, W_max);
+    if (ws_bytes < f.need) return MVB_ERR_WORKSPACE;
+    mvbk::FusedParams F = {};
+    mvbk::SegParams& S = F.S;
+    S.in = p.in;
+    S.mis = p.mis;
+    S.len = p.len;
+    S.count = p.count;
+    S.out = p.out;
+    S.prev = p.prev;
+    S.prev_dev = p.prev_dev;
+    S.seg_bytes = mvbk::kUnit;
+    S.n_seg = f.n_seg;
+    S.hdr = p.hdr;
+    S.res_dev = p.res_dev;
+    F.swz = g_fused_swz;
+    F.levels = f.levels;
+    char* b = static_cast<char*>(ws) + kHeaderBytes;
+    for (int l = 0; l < f.levels; ++l) {
+        F.n_at[l] = f.n_at[l];
+        F.tree[l] = reinterpret_cast<mvbk::FEntry*>(b);
+        b += sizeof(mvbk::FEntry) * static_cast<size_t>(f.n_at[l]);
+        F.arrive[l] = l ? reinterpret_cast<unsigned*>(b) : nullptr;
+        b += l ? 4 * static_cast<size_t>(f.n_at[l]) : 0;
+        b = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(b) + 15) & ~static_cast<uintptr_t>(15));
+    }
+    const unsigned long long layout = (6ull << 56) ^ static_cast<unsigned long long>(f.n_seg);
+    if (prepare_workspace(ws, f.need, layout, s) != cudaSuccess) return MVB_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(f.W / mvbk::kSegWarps));
+    cfg.blockDim = dim3(mvbk::kSegThreads);
+    cfg.dynamicSmemBytes = mvbk::kFSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta>, F) != cudaSuccess) return MVB_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
 // Persistent warp-sliced launch (decode_v3.cuh).
 template <bool Delta>
 cudaError_t launch_v3(const mvbk::WParams& p, cudaStream_t s) {
@@ -413,6 +524,8 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.trace = trace;
 
     if (mode == MVB_STRICT && g_kernel_choice == 0 && trace == nullptr)
+        return delta ? launch_fused<true>(p, ws, ws_bytes, stream) : launch_fused<false>(p, ws, ws_bytes, stream);
+    if (mode == MVB_STRICT && g_kernel_choice == 6 && trace == nullptr)
         return delta ? launch_seg<true, 1>(p, ws, ws_bytes, stream) : launch_seg<false, 1>(p, ws, ws_bytes, stream);
     if (mode == MVB_STRICT && g_kernel_choice == 5 && trace == nullptr)
         return delta ? launch_seg<true, 0>(p, ws, ws_bytes, stream) : launch_seg<false, 0>(p, ws, ws_bytes, stream);
@@ -696,7 +809,11 @@ size_t mvb_workspace_bytes(size_t in_len) {
     // segmented decode with 1 KiB segments (the finest any launch uses)
     const size_t n_seg = (in_len + 15) / 1024 + 1, n_grp = n_seg / 32 + 1, n_sup = n_grp / 32 + 1;
     const size_t c = kHeaderBytes + 8 * n_seg + 16 * n_grp + 16 * n_sup;
-    return std::max(std::max(a, b), c);
+    // fused decode (fused_plan): 1 KiB segments at the finest, a 32-ary tree
+    // of 16-byte entries (+ 4-byte arrival counters above level 0)
+    const size_t fs = (in_len + 15) / mvbk::kUnit + 2;
+    const size_t d = kHeaderBytes + 16 * fs + 20 * (fs / 31 + 2 * mvbk::kFLevels) + 16 * mvbk::kFLevels;
+    return std::max(std::max(a, b), std::max(c, d));
 }
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
@@ -1056,7 +1173,7 @@ void mvbx_set_host_pipeline(size_t min_bytes, size_t chunk_bytes, int grow) {
 // Kernels one decode call launches in steady state (bench accounting; the
 // workspace re-zeroing memset runs only when a workspace changes layout).
 int mvbx_kernels_per_decode(int mode) {
-    return (mode == MVB_STRICT && (g_kernel_choice == 0 || g_kernel_choice == 5)) ? 2 : 1;
+    return (mode == MVB_STRICT && (g_kernel_choice == 5 || g_kernel_choice == 6)) ? 2 : 1;
 }
 
 const char* mvb_version(void) { return "mvb_cuda 0.2 (sm_100a, segmented lane-local VByte decoder)"; }
