@@ -121,9 +121,12 @@ __device__ __forceinline__ uint4 ldg_keep16(const void* p, unsigned long long po
 // Terminator count (inside the stream) and, for delta, digit-weight sum of
 // the segment bytes [q0, q1) (1 KiB iterations; lane l: bytes 32l .. 32l+31
 // of each).  Identical in every lane on return.
+// flags_out bit 0 (delta): some byte follows three or more continuation bytes
+// (an integer of 4+ bytes, or a malformed run).
 template <bool kDelta>
 __device__ __forceinline__ void fused_totals(const SegParams& S, long long q0, long long q1, int lane,
-                                             unsigned& cnt_out, uint32_t& sum_out, uint32_t ubuf = 0u) {
+                                             unsigned& cnt_out, uint32_t& sum_out, uint32_t ubuf = 0u,
+                                             uint32_t* flags_out = nullptr) {
     const uint8_t* const ab = S.in - S.mis;
     const long long qlo = S.mis, qhi = S.mis + S.len;
     // ubuf: shared-memory address of byte q0 (the whole range and the 16 bytes
@@ -139,7 +142,7 @@ __device__ __forceinline__ void fused_totals(const SegParams& S, long long q0, l
     }
     unsigned tc = 0;      // terminators counted directly (edge iterations) + 32 per interior iteration
     uint32_t cc = 0;      // 128 x continuation bytes of interior iterations
-    uint32_t sA = 0, sB = 0, sX = 0;
+    uint32_t sA = 0, sB = 0, sX = 0, flags = 0;
     long long q = q0;
     const unsigned long long pol = l2_evict_last();
     uint4 x0, x1;
@@ -197,6 +200,7 @@ __device__ __forceinline__ void fused_totals(const SegParams& S, long long q0, l
 #pragma unroll
             for (int k = 1; k < 8; ++k) ftot_word(w[k], w[k - 1], ccx, a, b, hi3);
             if (__any_sync(0xFFFFFFFFu, hi3 != 0)) {  // an integer of 4+ bytes: the exact weights
+                flags |= 1u;
                 uint32_t s = ftot_word_exact(w[0], p1, p2) + ftot_word_exact(w[1], w[0], p1);
 #pragma unroll
                 for (int k = 2; k < 8; ++k) s += ftot_word_exact(w[k], w[k - 1], w[k - 2]);
@@ -211,6 +215,7 @@ __device__ __forceinline__ void fused_totals(const SegParams& S, long long q0, l
             for (int k = 0; k < 8; ++k) cc = __dp4a(w[k] & 0x80808080u, 0x01010101u, cc);
         }
     }
+    if (flags_out) *flags_out = flags;
     unsigned cnt = tc - (cc >> 7);
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
     uint32_t sum = 0;
@@ -271,11 +276,13 @@ __device__ __forceinline__ void slot_store(uint32_t& sp, uint32_t T, uint32_t bi
 // wp3: the 4 bytes before the lane; w: its 32 bytes; T: its in-range
 // terminators (bit j = byte j); sp: staging address of its first output;
 // carry (in/out, warp-uniform): the byte-convention carry before the slice.
+// The word totals are independent dp2a pairs, so each word's outputs hang off
+// its own base (short dependency chains instead of one chain of 16 dp2a).
 template <bool kSwz>
 __device__ __forceinline__ void lane_slots_d3(uint32_t wp3, const uint32_t (&w)[8], uint32_t T, uint32_t sp,
                                               uint32_t& carry) {
-    uint32_t W01[8], W23[8], w7[8];
-    uint32_t tot = 0, prev = wp3;
+    uint32_t W01[8], W23[8], w7[8], tk[8];
+    uint32_t prev = wp3;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t s8 = __funnelshift_l(prev, w[k], 8), s16 = __funnelshift_l(prev, w[k], 16);
@@ -285,20 +292,63 @@ __device__ __forceinline__ void lane_slots_d3(uint32_t wp3, const uint32_t (&w)[
         W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
         W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
         w7[k] = w[k] & 0x7F7F7F7Fu;
-        tot = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], tot));
+        tk[k] = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], 0u));
         prev = w[k];
     }
+    uint32_t tot = tk[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) tot += tk[k];
     uint32_t acc = lane_scan_offset<true>(tot, carry);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
         const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
         const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
-        acc = dp2a_hi(W23[k], w7[k], o1);
+        acc += tk[k];
         slot_store<kSwz>(sp, T, 1u << (4 * k), o0);
         slot_store<kSwz>(sp, T, 2u << (4 * k), o1);
         slot_store<kSwz>(sp, T, 4u << (4 * k), o2);
         slot_store<kSwz>(sp, T, 8u << (4 * k), acc);
+    }
+}
+
+// A delta unit staged in shared memory whose integers all have at most 3
+// bytes, with integer limit-1 outside it (both known from its totals pass):
+// every slice takes the dp2a path with no range masks, votes or limit checks.
+// carry: every byte before the unit (the prefix tree's sums count bytes, so
+// no straddle correction); values go to out[base ...].
+template <bool kSwz>
+__device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, int n_slices, unsigned long long base, uint32_t carry,
+                                               unsigned long long limit, uint32_t* out, uint32_t* stage, int lane) {
+    const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
+    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    unsigned long long run = base;
+    uint32_t pw = 0;  // lane 0: the 4 bytes before the slice
+    if (lane == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(ubuf - 4u) : "memory");
+#pragma unroll 1
+    for (int i = 0; i < n_slices; ++i) {
+        const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
+        const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * i + 32 * lane);
+        const uint4 x0 = lds128(sa), x1 = lds128(sa + 16u);
+        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1);
+        const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31);
+        if (lane == 0) wp3 = pw;
+        pw = l3;
+        const uint32_t T32 = hibits16(~w[0], ~w[1], ~w[2], ~w[3]) | (hibits16(~w[4], ~w[5], ~w[6], ~w[7]) << 16);
+        const uint32_t n_own = __popc(T32);
+        uint32_t incl = n_own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        lane_slots_d3<kSwz>(wp3, w, T32, st_base + 4u * (a + incl - n_own), carry);
+        __syncwarp();
+        stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
+        run += n_w;
+        __syncwarp();  // the staging buffer is rewritten by the next slice
     }
 }
 
@@ -675,13 +725,14 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     // tickets before it and published right after, so its prefix is out).
     long long up = -1;  // the unit awaiting its decode (buffer bp)
     int bp = 0;
+    unsigned c_up = 0;  // its totals pass: integer count, flags
+    uint32_t f_up = 0;
+    unsigned c_u = 0;
+    uint32_t f_u = 0;
     for (;;) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
         const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
-        // output index and carry of unit up (loads overlap the ticket's)
-        unsigned long long base = 0, csum = 0;
-        if (up >= 0) fused_prefix(F, up, tag, lane, base, csum);
         if (u < S.n_seg) {
             const int b = bp ^ 1;
             const long long qs = u * kUnit;
@@ -693,41 +744,50 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 }
                 phases ^= 1u << b;
             }
-            unsigned c;
             uint32_t su;
-            fused_totals<kDelta>(S, qs, qs + kUnit, lane, c, su, ubuf);
-            fused_publish(F, 0, u, c, su, tag, lane);
+            fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, ubuf, &f_u);
+            fused_publish(F, 0, u, c_u, su, tag, lane);
         }
+        // output index and carry of unit up -- only now: a wait here must never
+        // hold back the publication of unit u, which later units wait for
+        unsigned long long base = 0, csum = 0;
+        if (up >= 0) fused_prefix(F, up, tag, lane, base, csum);
         if (up >= 0 && base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
             const long long qs = up * kUnit;
             const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
-            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;
+            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
             const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
-            uint32_t straddle = 0;
-            if (kDelta) {
-                uint32_t wb;
-                if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
-                else wb = r_word(R, qs - 4);
-                straddle = shr_clamp(pack28(wb), 7 * (32 - __clz(static_cast<int>(hibits4(~wb)))));
+            const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
+            if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
+                // every integer has at most 3 bytes, integer count-1 ends after the
+                // unit: the dp2a path throughout (carry: every byte before the unit)
+                const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
+                if (swz)
+                    decode_unit_d3<true>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
+                else
+                    decode_unit_d3<false>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
+            } else {
+                uint32_t straddle = 0;
+                if (kDelta) {
+                    uint32_t wb;
+                    if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
+                    else wb = r_word(R, qs - 4);
+                    straddle = tail_value(wb);
+                }
+                const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
+                RangeOut ro;
+                if (swz)
+                    decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
+                else
+                    decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
             }
-            const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
-            bool swz = F.swz == 1;
-            if (F.swz == 2) {
-                unsigned long long n_own;
-                uint32_t unused;
-                fentry_get(F.tree[0] + up, tag, n_own, unused);
-                swz = range_dense(n_own, qe - qs);
-            }
-            RangeOut ro;
-            if (swz)
-                decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
-            else
-                decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
             __syncwarp();  // (buffer bp is refilled next iteration)
         }
         if (u >= S.n_seg) break;
         up = u;
         bp ^= 1;
+        c_up = c_u;
+        f_up = f_u;
     }
     fused_complete(F, tag);
 }

@@ -1,0 +1,4 @@
+O=gpurun_out/r2_t15
+mkdir -p $O
+for c in c4 c2 c5_p50_delta; do python scripts/r2/sweep_chunk.py $c u4k:0; done > $O/sweep.txt 2>&1
+for v in u2k u8k; do for c in c4 c2; do MVB_CUDA_LIB=build_variants/libmvb_$v.so python scripts/r2/sweep_chunk.py $c $v:0; done; done >> $O/sweep.txt 2>&1; cat $O/sweep.txt

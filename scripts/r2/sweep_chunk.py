@@ -19,8 +19,11 @@ if has_set:
     L.mvbx_set_fused.argtypes = [ctypes.c_size_t, ctypes.c_longlong]
 exp = torch.from_numpy(w.expected().view(np.int32)).to(dev)
 for arg in sys.argv[2:]:
-    seg, lag = (int(x) for x in arg.split(":"))
-    if has_set:
+    try:
+        seg, lag = (int(x) for x in arg.split(":"))
+    except ValueError:  # a label (library variant runs)
+        seg, lag = arg, 0
+    if has_set and isinstance(seg, int):
         L.mvbx_set_fused(seg, lag)
     def step(i):
         k = i % R
