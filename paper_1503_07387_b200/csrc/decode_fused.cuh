@@ -537,7 +537,10 @@ __device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long 
         const long long par = i >> 5;
         const unsigned kids = static_cast<unsigned>((F.n_at[l] - (par << 5)) < 32 ? F.n_at[l] - (par << 5) : 32);
         unsigned last = 0;
-        if (lane == 0) last = (atomicAdd(F.arrive[l + 1] + par, 1u) + 1u) % kids == 0u ? 1u : 0u;
+        if (lane == 0) {
+            const unsigned n = atomicAdd(F.arrive[l + 1] + par, 1u) + 1u;
+            last = (kids == 32u ? (n & 31u) : n % kids) == 0u ? 1u : 0u;
+        }
         last = __shfl_sync(0xFFFFFFFFu, last, 0);
         if (!last) return;
         unsigned long long c = 0;
@@ -578,6 +581,51 @@ __device__ __forceinline__ void fused_prefix(const FusedParams& F, long long v, 
     }
     cnt = c;
     sum = s;
+}
+
+// fused_totals for a unit staged in shared memory (ubuf: its first byte; the
+// 16 bytes before it are there too): n_it 1 KiB iterations, all inside the
+// stream -- no range masks, 32-bit addressing.
+template <bool kDelta>
+__device__ __forceinline__ void unit_totals(uint32_t ubuf, int n_it, int lane, unsigned& cnt_out, uint32_t& sum_out,
+                                            uint32_t& flags_out) {
+    uint32_t h1 = 0;  // lane 0: the word before the iteration
+    if (lane == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(h1) : "r"(ubuf - 4u) : "memory");
+    uint32_t cc = 0, sA = 0, sB = 0, sX = 0, flags = 0;
+#pragma unroll 1
+    for (int it = 0; it < n_it; ++it) {
+        const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * it + 32 * lane);
+        const uint4 x0 = lds128(sa), x1 = lds128(sa + 16u);
+        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        uint32_t p1 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1);
+        const uint32_t l1 = __shfl_sync(0xFFFFFFFFu, w[7], 31);
+        if (lane == 0) p1 = h1;
+        h1 = l1;
+        if (kDelta) {
+            uint32_t hi3 = 0, a = 0, b = 0;
+            ftot_word(w[0], p1, cc, a, b, hi3);
+#pragma unroll
+            for (int k = 1; k < 8; ++k) ftot_word(w[k], w[k - 1], cc, a, b, hi3);
+            if (__any_sync(0xFFFFFFFFu, hi3 != 0)) {  // an integer of 4+ bytes: the exact weights
+                flags |= 1u;
+                uint32_t p2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
+                if (lane == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(p2) : "r"(sa - 8u) : "memory");
+                uint32_t x = ftot_word_exact(w[0], p1, p2) + ftot_word_exact(w[1], w[0], p1);
+#pragma unroll
+                for (int k = 2; k < 8; ++k) x += ftot_word_exact(w[k], w[k - 1], w[k - 2]);
+                sX += x;
+            } else {
+                sA += a;
+                sB += b;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cc = __dp4a(w[k] & 0x80808080u, 0x01010101u, cc);
+        }
+    }
+    flags_out = flags;
+    cnt_out = __reduce_add_sync(0xFFFFFFFFu, 32u * static_cast<unsigned>(n_it) - (cc >> 7));
+    sum_out = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sA + (sB << 14) + sX) : 0u;
 }
 
 // Completion (all threads of every CTA): the last CTA produces the DecodeResult.
@@ -723,69 +771,77 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     // Pipeline per warp: take unit u, load it, total it and publish -- then
     // decode the unit taken one iteration earlier (its predecessors took their
     // tickets before it and published right after, so its prefix is out).
+    // The publication must follow the ticket closely: a unit is waited for by
+    // every later one.  (Taking the ticket before the previous unit's decode,
+    // to overlap the load with it, made later units wait a whole decode.)
     long long up = -1;  // the unit awaiting its decode (buffer bp)
     int bp = 0;
     unsigned c_up = 0;  // its totals pass: integer count, flags
     uint32_t f_up = 0;
-    unsigned c_u = 0;
-    uint32_t f_u = 0;
     for (;;) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
         const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+        const int b = bp ^ 1;
+        unsigned c_u = 0;
+        uint32_t f_u = 0;
         if (u < S.n_seg) {
-            const int b = bp ^ 1;
             const long long qs = u * kUnit;
             const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
-            const uint32_t ubuf = staged ? buf0 + b * kUnitBuf + 16u : 0u;
+            uint32_t su;
             if (staged) {
                 if (lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qs - 16, kUnit + 16, bar0 + 8u * b);
                 while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
                 }
                 phases ^= 1u << b;
+                unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+            } else {
+                fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
             }
-            uint32_t su;
-            fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, ubuf, &f_u);
             fused_publish(F, 0, u, c_u, su, tag, lane);
         }
-        // output index and carry of unit up -- only now: a wait here must never
-        // hold back the publication of unit u, which later units wait for
-        unsigned long long base = 0, csum = 0;
-        if (up >= 0) fused_prefix(F, up, tag, lane, base, csum);
-        if (up >= 0 && base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
-            const long long qs = up * kUnit;
-            const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
-            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
-            const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
-            const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
-            if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
-                // every integer has at most 3 bytes, integer count-1 ends after the
-                // unit: the dp2a path throughout (carry: every byte before the unit)
-                const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
-                if (swz)
-                    decode_unit_d3<true>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
-                else
-                    decode_unit_d3<false>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
-            } else {
-                uint32_t straddle = 0;
-                if (kDelta) {
-                    uint32_t wb;
-                    if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
-                    else wb = r_word(R, qs - 4);
-                    straddle = tail_value(wb);
+        // ---- decode unit up (only now: a wait here must never hold back the
+        // publication of unit u, which later units wait for) ----
+        if (up >= 0) {
+            unsigned long long base, csum;
+            fused_prefix(F, up, tag, lane, base, csum);
+            if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
+                const long long qs = up * kUnit;
+                const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
+                const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
+                const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
+                const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
+                if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
+                    // every integer has at most 3 bytes, integer count-1 ends after the
+                    // unit: the dp2a path throughout (carry: every byte before the unit)
+                    const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
+                    if (swz)
+                        decode_unit_d3<true>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
+                    else
+                        decode_unit_d3<false>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
+                } else {
+                    uint32_t straddle = 0;
+                    if (kDelta) {
+                        uint32_t wb;
+                        if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
+                        else wb = r_word(R, qs - 4);
+                        straddle = tail_value(wb);
+                    }
+                    const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
+                    RangeOut ro;
+                    if (swz)
+                        decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                     ro);
+                    else
+                        decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                      ro);
                 }
-                const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
-                RangeOut ro;
-                if (swz)
-                    decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
-                else
-                    decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K, ro);
             }
             __syncwarp();  // (buffer bp is refilled next iteration)
         }
         if (u >= S.n_seg) break;
         up = u;
-        bp ^= 1;
+        bp = b;
         c_up = c_u;
         f_up = f_u;
     }
