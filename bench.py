@@ -1,28 +1,32 @@
 """Benchmark of the B200 VByte decoder (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
-A step is one decode of one synthetic stream (BASELINE.json configs[1] by
-default: delta decode of 2^24 gaps, 50% 1-byte / 50% 2-byte).  `value` is
-decoded integers per second over all ranks with inputs resident in HBM; `e2e`
-is the same metric through the host-pointer C-ABI drop-in
-(mvb_decode_delta_stream) with pinned host buffers, H2D and D2H inside the
-timed region.  L2 residency is defeated by rotating 4 input/output buffer
-sets whose total (4 x 92 MB for c2) is well above the 126 MB L2.
+A step is one decode of one synthetic stream.  The default is BASELINE.json
+configs[3] (c4): delta decode of 2^30 gaps (geometric, mean 3, plus 1% of
+3-byte gaps), the largest config that fits one GPU and the one the north
+star's scaling target names.  `value` is decoded integers per second over
+all ranks with the input resident in HBM (the input, 1.1 GB, and the output,
+4.3 GB, are both far larger than the 126 MB L2); `e2e` is the same metric
+through the host-pointer C-ABI drop-in (mvb_decode_delta_stream) with pinned
+host buffers, H2D and D2H inside the timed region.
 
-Multi-GPU (torchrun): configs c1/c2/c5 are independent replicas per rank
-(weak scaling, no data-path collective).  --config c4 is the
-sharded config: one 2^30-integer delta stream split by byte range across the
-ranks (strong scaling): per step a totals pre-pass, one NCCL all-gather of a
+Multi-GPU (torchrun): c4 is split by byte range across the ranks (strong
+scaling): per step a totals pass over the shard, one NCCL all-gather of a
 16-byte record per rank, a carry kernel and the decode, all on-stream.
+c1/c2/c5 run independent replicas per rank (weak scaling, no data-path
+collective); c3 partitions the lists into contiguous ranges
+balanced by compressed bytes (weak in bytes per rank, no collective).
 Timing is CUDA events with barrier + synchronize on both sides and the max
 over ranks.
 
 --impl reference times the reference's own CPU decoder (oracle/_ref, the
-unmodified reference library built from its sources) on this host's cores:
-one stream per thread, as many threads as the host has, each decoding its
-own replica of the same stream (the reference cannot split one stream,
-SPEC.md:360).
+unmodified reference library built from its sources) on this host's cores,
+on the same config: one stream per thread, as many threads as the host has,
+each decoding its own replica of a bounded sample of the same stream (the
+reference cannot split one stream).  Its input bytes come from
+the reference's own encoder; the values are generated in a child process so
+that the timed process maps no library of ours.
 """
 from __future__ import annotations
 
@@ -57,14 +61,47 @@ def load_peaks():
 
 
 def load_ncu_traffic(workload):
-    """dram bytes per launch of the decode kernel from the committed ncu summary."""
+    """DRAM bytes (read + write) per launch of the decode kernel on this
+    workload, from the committed ncu --set full summary of the current build
+    (profiles/r02/ncu_traffic.json; null if the workload was not captured)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")) as f:
             d = json.load(f)
         v = d.get(workload)
-        return float(v) if v is not None else None
+        return float(v["dram_bytes_per_launch"]) if v is not None else None
     except Exception:
         return None
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def config_dict(name, count, in_bytes, bytes_per_int, delta, world, lists=None):
+    """The `config` object of both arms (identical for the same config and N)."""
+    d = {"workload": name, "n": int(count), "in_bytes": int(in_bytes), "bytes_per_int": round(float(bytes_per_int), 4),
+         "delta": bool(delta)}
+    if lists is not None:
+        d["lists"] = int(lists)
+    if name.startswith("c4"):
+        d["parallelism"] = f"byte-range shards x{world}" if world > 1 else "single"
+    elif lists is not None:
+        d["parallelism"] = f"list ranges x{world}" if world > 1 else "single"
+    else:
+        d["parallelism"] = f"replicas x{world}" if world > 1 else "single"
+    total = int(in_bytes) + 4 * int(count)
+    d["l2"] = (f"inputs larger than L2 ({total / 1e6:.0f} MB in + out > 126 MB)" if total > 4 * 126_000_000 else
+               f"rotating 4 input/output sets ({4 * total / 1e6:.0f} MB > 126 MB L2)")
+    return d
 
 
 def make_workload(name):
@@ -184,60 +221,141 @@ def dist_setup(args):
     return world, rank, local
 
 
+SAMPLE_INTS = 1 << 26  # reference arm / cpu_baseline sample of a long stream: its first 2^26 integers
+
+
+def emit_values(cfg: str) -> None:
+    """(child process of the reference arm) Generate workload `cfg` and write a
+    JSON header line plus the raw sample: the first SAMPLE_INTS values (or gaps)
+    of a stream, or every list's gaps and the int offsets of a batch."""
+    w = make_workload(cfg)
+    lists = None if w.int_offsets is None else int(w.int_offsets.size - 1)
+    k = w.count if lists is not None else min(w.count, SAMPLE_INTS)
+    h = {"name": w.name, "count": w.count, "in_bytes": int(w.encoded.size), "bytes_per_int": w.bytes_per_int,
+         "delta": w.delta, "prev": int(w.prev), "k": int(k), "lists": lists}
+    out = sys.stdout.buffer
+    out.write((json.dumps(h) + "\n").encode())
+    out.write(np.ascontiguousarray(w.values[:k], dtype=np.uint32).tobytes())
+    if lists is not None:
+        out.write(np.ascontiguousarray(w.int_offsets, dtype=np.uint64).tobytes())
+    out.flush()
+
+
+def reference_input(cfg: str):
+    """The reference arm's input: values from a child process (so this process
+    maps no library of ours), bytes from the reference's own encoder."""
+    import subprocess
+
+    from oracle import RefLib
+
+    p = subprocess.run([sys.executable, os.path.abspath(__file__), "--emit-values", cfg], capture_output=True,
+                       check=True)
+    nl = p.stdout.index(b"\n")
+    h = json.loads(p.stdout[:nl])
+    body = memoryview(p.stdout)[nl + 1:]
+    k = h["k"]
+    vals = np.frombuffer(body[:4 * k], dtype=np.uint32)
+    io = None
+    if h["lists"] is not None:
+        io = np.frombuffer(body[4 * k:4 * k + 8 * (h["lists"] + 1)], dtype=np.uint64)
+    ref = RefLib()
+    enc = ref.encode_sequence(vals)  # VByte is per integer: the lists' concatenation is one stream
+    bo = None
+    if io is not None:
+        sizes = (1 + (vals >= 1 << 7).astype(np.uint8) + (vals >= 1 << 14) + (vals >= 1 << 21) + (vals >= 1 << 28))
+        cum = np.zeros(vals.size + 1, np.uint64)
+        np.cumsum(sizes, dtype=np.uint64, out=cum[1:])
+        bo = cum[io.astype(np.int64)]
+    return h, vals, enc, bo, io
+
+
 def run_reference(args):
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return
-    w = make_workload(args.config)
-    if w.byte_offsets is not None:  # c3: lists split over all host threads, each step a bounded sample
-        threads = os.cpu_count() or 1
-        cpu_lists_rate(w, 0.0, 1, gate=True)
-        t_steps, ints = [], 0
-        for _ in range(args.steps):
-            rate, _, n_ints = cpu_lists_rate(w, 0.5, threads, gate=False)
-            t_steps.append(n_ints / rate)
-            ints += n_ints
-        value = ints / sum(t_steps) / 1e9
-        line = {
-            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.count, "lists": int(w.byte_offsets.size - 1),
-                       "in_bytes": int(w.encoded.size), "bytes_per_int": w.bytes_per_int},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"each step: ~0.5 s of list decodes (mvb::decode_delta_stream per list, "
-                                       f"lists split over {threads} threads)"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
-        return
-    if w.count > (1 << 26):  # bounded sample per thread: the first 2^26 integers of the stream
-        from paper_1503_07387_b200 import workload as W
+    from oracle import RefLib
 
-        k = 1 << 26
-        w = W.Workload(w.name, w.delta, w.values[:k], w.encoded[:int(W.encode(w.values[:k]).size)], prev=w.prev)
+    ref = RefLib()
+    h, vals, enc, bo, io = reference_input(args.config)
     threads = os.cpu_count() or 1
-    # each step: every host thread decodes one replica (bounded: ~ a few s total)
-    rates = []
-    cpu_reference_rate(w, 0.0, 1, gate=True)
-    for _ in range(args.warmup):
-        cpu_reference_rate(w, 0.0, threads, gate=False)
-    t_steps = []
-    for _ in range(args.steps):
-        rate, reps = cpu_reference_rate(w, 0.0, threads, gate=False)
-        t_steps.append(reps * w.count / rate)
-        rates.append(rate)
-    value = w.count * threads * args.steps / sum(t_steps) / 1e9
+    model = cpu_model()
+    cfg = config_dict(h["name"], h["count"], h["in_bytes"], h["bytes_per_int"], h["delta"], args.gpus, h["lists"])
+    if io is not None:  # c3: lists split over all host threads, each step a bounded sample
+        out = np.empty(vals.size + 16, np.uint32)
+        n = io.size - 1
+        cuts = np.linspace(0, n, threads + 1).astype(np.int64)
+        assert ref.decode_delta_lists(enc, bo, io, out, 0, n) == 0
+        exp_ok = all(np.array_equal(out[int(io[i]):int(io[i]) + 3],
+                                    np.cumsum(vals[int(io[i]):int(io[i]) + 3], dtype=np.uint64).astype(np.uint32))
+                     for i in range(0, n, max(1, n // 64)))
+        assert exp_ok, "reference list decode disagrees with ground truth"
+
+        def step(seconds):
+            done, ints = [0] * threads, [0] * threads
+            stop_at = time.perf_counter() + seconds
+
+            def work(i):
+                lo, hi = int(cuts[i]), int(cuts[i + 1])
+                while True:
+                    assert ref.decode_delta_lists(enc, bo, io, out, lo, hi) == 0
+                    ints[i] += int(io[hi] - io[lo])
+                    if time.perf_counter() >= stop_at:
+                        break
+
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            return sum(ints), time.perf_counter() - t0
+
+        for _ in range(args.warmup):
+            step(0.0)
+        t_steps, n_ints = [], 0
+        for _ in range(args.steps):
+            k, dt = step(0.5)
+            n_ints += k
+            t_steps.append(dt)
+        value = n_ints / sum(t_steps) / 1e9
+        sample = (f"each step: ~0.5 s of list decodes (mvb::decode_delta_stream per list, runner.cpp decode_list), "
+                  f"lists split over {threads} threads")
+    else:
+        k = vals.size
+        outs = [np.empty(k + 16, np.uint32) for _ in range(threads)]
+        dec = (lambda o: ref.decode_delta_stream(enc, k, h["prev"], out=o)) if h["delta"] else \
+            (lambda o: ref.decode_stream(enc, k, out=o))
+        r, o = dec(outs[0])  # correctness gate (runner.cpp:147-165)
+        exp = (np.cumsum(vals, dtype=np.uint64) + np.uint64(h["prev"])).astype(np.uint32) if h["delta"] else vals
+        assert r[0] == 0 and r[1] == k and np.array_equal(o, exp), "reference decode disagrees with ground truth"
+
+        def step():
+            def work(i):
+                r, _ = dec(outs[i])
+                assert r[0] == 0
+
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            return time.perf_counter() - t0
+
+        for _ in range(args.warmup):
+            step()
+        t_steps = [step() for _ in range(args.steps)]
+        value = k * threads * args.steps / sum(t_steps) / 1e9
+        sample = (f"each step: {threads} threads x 1 decode of the first {k} integers of the {h['name']} stream "
+                  f"(reference encoder's bytes) with mvb::decode{'_delta' if h['delta'] else ''}_stream "
+                  "(SSE masked path)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": {"workload": w.name, "n": w.count, "in_bytes": int(w.encoded.size),
-                                        "bytes_per_int": w.bytes_per_int},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"each step: {threads} threads x 1 full decode of the {w.name} stream "
-                                   f"({w.count} ints) with mvb::decode{'_delta' if w.delta else ''}_stream "
-                                   "(SSE masked path)"},
+        "higher_is_better": True, "scaling": "strong" if h["name"].startswith("c4") else "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                         "cpu_model": model},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -360,7 +478,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         try:
             rate, reps = cpu_reference_rate(w, args.cpu_seconds, 1)
-            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"{reps} full decodes of the {w.name} stream ({count} ints) by the reference "
                              f"library's decode{'_delta' if w.delta else ''}_stream (SSE masked path), 1 thread, "
                              f"~{args.cpu_seconds:.0f} s"}
@@ -372,10 +490,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": w.name, "n": count, "in_bytes": in_len,
-                       "bytes_per_int": round(w.bytes_per_int, 4), "delta": w.delta,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single",
-                       "l2": f"rotating {R} input/output sets ({R * (in_len + 4 * count) / 1e6:.0f} MB > 126 MB L2)"},
+            "config": config_dict(w.name, count, in_len, w.bytes_per_int, w.delta, world),
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac_of_nominal_8000": achieved / NOMINAL_HBM_GBS,
@@ -531,7 +646,8 @@ def run_sharded(args):
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         try:
             rate, reps, sample = cpu_reference_sample(w, args.cpu_seconds, 1)
-            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample}
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample,
+                   "cpu_model": cpu_model()}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -540,10 +656,7 @@ def run_sharded(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.count, "in_bytes": L, "bytes_per_int": round(w.bytes_per_int, 4),
-                       "delta": w.delta, "parallelism": f"byte-range shards x{world}" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (rank 0 shard {shard_bytes / 1e6:.0f} MB in + "
-                             f"{4 * n_local / 1e6:.0f} MB out > 126 MB)"},
+            "config": config_dict(w.name, w.count, L, w.bytes_per_int, w.delta, world),
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac_of_nominal_8000": achieved / NOMINAL_HBM_GBS,
@@ -604,12 +717,14 @@ def cpu_lists_rate(w, seconds, threads, gate=True):
 def run_lists(args):
     """Config 3: 65,536 independent delta-coded posting lists decoded in one
     launch (mvb_decode_delta_lists_device, one warp per list, longest first).
-    A step decodes the whole batch.  Multi-GPU: replicas (the
-    lists partition with no exchange; each rank decodes a full batch)."""
+    A step decodes the whole batch.  Multi-GPU: each rank decodes a contiguous
+    range of lists balanced by compressed bytes (shard.list_ranges; SURVEY.md
+    §8e: independent units, no exchange) -- the batch is split, not replicated."""
     import torch
     import torch.distributed as dist
 
     from paper_1503_07387_b200 import _lib, mvb
+    from paper_1503_07387_b200.shard import list_ranges
 
     world, rank, local = dist_setup(args)
     if world > 1:
@@ -618,27 +733,36 @@ def run_lists(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     w = make_workload(args.config)
-    n_lists = w.byte_offsets.size - 1
-    lens = np.diff(w.byte_offsets.astype(np.int64))
+    n_all = w.byte_offsets.size - 1
+    cuts = list_ranges(w.byte_offsets, world)
+    l0, l1 = cuts[rank], cuts[rank + 1]
+    bo_all = w.byte_offsets.astype(np.int64)
+    io_all = w.int_offsets.astype(np.int64)
+    b0, b1, i0, i1 = int(bo_all[l0]), int(bo_all[l1]), int(io_all[l0]), int(io_all[l1])
+    n_lists, n_ints, n_bytes = l1 - l0, i1 - i0, b1 - b0
+    bo_r = (bo_all[l0:l1 + 1] - b0).astype(np.uint64)
+    io_r = (io_all[l0:l1 + 1] - i0).astype(np.uint64)
+    lens = np.diff(bo_r.astype(np.int64))
     order_np = np.argsort(-lens, kind="stable").astype(np.uint32)
-    h_in = torch.from_numpy(w.encoded).pin_memory()
-    h_bo = torch.from_numpy(w.byte_offsets.astype(np.uint64).view(np.int64)).pin_memory()
-    h_io = torch.from_numpy(w.int_offsets.astype(np.uint64).view(np.int64)).pin_memory()
+    h_in = torch.from_numpy(np.ascontiguousarray(w.encoded[b0:b1])).pin_memory()
+    h_bo = torch.from_numpy(bo_r.view(np.int64)).pin_memory()
+    h_io = torch.from_numpy(io_r.view(np.int64)).pin_memory()
     src, bo, io = h_in.to(dev), h_bo.to(dev), h_io.to(dev)
     order = torch.from_numpy(order_np.view(np.int32)).to(dev)
-    out = torch.empty(w.count, dtype=torch.int32, device=dev)
-    res = torch.zeros(n_lists * 3, dtype=torch.int64, device=dev)
+    out = torch.empty(max(n_ints, 1), dtype=torch.int32, device=dev)
+    res = torch.zeros(max(n_lists, 1) * 3, dtype=torch.int64, device=dev)
     d = mvb.Decoder(dev, 1 << 12)
     stream = torch.cuda.current_stream(dev)
+    expected = w.expected()[i0:i1]
 
     def step():
-        d.decode_lists(src, bo, io, out, order=order, results=res, delta=True)
+        d.decode_lists(src, bo, io, out[:n_ints], order=order, results=res, delta=True)
 
     step()
     torch.cuda.synchronize()
-    rr = res.cpu().numpy().reshape(-1, 3)
-    assert (rr[:, 0] == 0).all() and (rr[:, 1] == np.diff(w.int_offsets.astype(np.int64))).all(), "list results"
-    assert torch.equal(out, torch.from_numpy(w.expected().view(np.int32)).to(dev)), "batched list decode mismatch"
+    rr = res.cpu().numpy().reshape(-1, 3)[:n_lists]
+    assert (rr[:, 0] == 0).all() and (rr[:, 1] == np.diff(io_r.astype(np.int64))).all(), "list results"
+    assert torch.equal(out[:n_ints], torch.from_numpy(expected.view(np.int32)).to(dev)), "batched list decode mismatch"
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -664,25 +788,25 @@ def run_lists(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = world * w.count * args.steps / (total_ms / 1e3) / 1e9
+    value = w.count * args.steps / (total_ms / 1e3) / 1e9  # every rank's lists: the whole batch per step
     meta = (n_lists + 1) * 16 + n_lists * 4 + n_lists * 24  # offsets, order, results
-    alg_bytes = int(w.encoded.size) + 4 * w.count + meta
+    alg_bytes = n_bytes + 4 * n_ints + meta
     achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
     peak, peak_kind = load_peaks()
 
     # end to end through the host-pointer batched entry (mvb_decode_delta_lists:
-    # pinned buffers; the stream, offsets and values cross PCIe every call, in
-    # pipelined sub-batches)
-    h_out = torch.empty(w.count, dtype=torch.int32).pin_memory()
+    # pinned buffers; this rank's bytes, offsets and values cross PCIe every
+    # call, in pipelined sub-batches)
+    h_out = torch.empty(max(n_ints, 1), dtype=torch.int32).pin_memory()
     Lh = _lib.lib()
 
     def e2e_step():
-        rc = Lh.mvb_decode_delta_lists(h_in.data_ptr(), int(w.encoded.size), h_bo.data_ptr(), h_io.data_ptr(),
-                                       None, n_lists, h_out.data_ptr(), 0, None)
+        rc = Lh.mvb_decode_delta_lists(h_in.data_ptr(), n_bytes, h_bo.data_ptr(), h_io.data_ptr(), None, n_lists,
+                                       h_out.data_ptr(), 0, None)
         assert rc == 0, rc
 
     e2e_step()
-    assert np.array_equal(h_out.numpy().view(np.uint32), w.expected()), "e2e output mismatch"
+    assert np.array_equal(h_out.numpy()[:n_ints].view(np.uint32), expected), "e2e output mismatch"
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -694,14 +818,14 @@ def run_lists(args):
     et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = world * w.count * e_steps / float(et.item()) / 1e9
+    e2e_value = w.count * e_steps / float(et.item()) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         try:
             threads = os.cpu_count() or 1
             rate, lists_done, ints_done = cpu_lists_rate(w, args.cpu_seconds, threads)
-            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+            cpu = {"value": rate / 1e9, "unit": UNIT, "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"{lists_done} list decodes ({ints_done} ints) of the {w.name} batch by the reference "
                              f"library's decode_delta_stream, one call per list (runner.cpp decode_list), lists "
                              f"split over {threads} host threads, ~{args.cpu_seconds:.0f} s"}
@@ -712,21 +836,18 @@ def run_lists(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": w.name, "n": w.count, "lists": n_lists, "in_bytes": int(w.encoded.size),
-                       "bytes_per_int": round(w.bytes_per_int, 4), "delta": True,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 ({(int(w.encoded.size) + 4 * w.count) / 1e6:.0f} MB > 126 MB)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config_dict(w.name, w.count, int(w.encoded.size), w.bytes_per_int, True, world, n_all),
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac_of_nominal_8000": achieved / NOMINAL_HBM_GBS, "frac": achieved / peak,
                          "traffic": load_ncu_traffic(w.name), "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
                          "kernel_ms_avg": statistics.mean(kern_ms), "kernel_ms_min": min(kern_ms),
-                         "kernel": "vbyte_lists_decode (one launch per batch)"},
+                         "kernel": "vbyte_lists_decode (one launch per batch; rank 0's list range)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(w.encoded.size) + 2 * (n_lists + 1) * 8,
-                    "d2h_bytes_per_step": 4 * w.count,
+                    "h2d_bytes_per_step": n_bytes + 2 * (n_lists + 1) * 8,
+                    "d2h_bytes_per_step": 4 * n_ints,
                     "api": "mvb_decode_delta_lists (host pointers, pinned, pipelined sub-batches)"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
@@ -796,7 +917,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--emit-values", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--preroll", type=float, default=1.0)
@@ -808,7 +930,9 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--min-ms", type=int, default=100)
     args = ap.parse_args()
-    if args.csv:
+    if args.emit_values:
+        emit_values(args.emit_values)
+    elif args.csv:
         run_csv(args)
     elif args.impl == "reference":
         run_reference(args)

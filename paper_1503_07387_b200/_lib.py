@@ -128,11 +128,11 @@ def kernels_per_decode(mode: int = 0) -> int:
 
 
 def set_kernel_choice(choice: int) -> None:
-    """Profiling/testing switch (internal symbol mvbx_set_kernel): strict-mode
-    kernel 0 = segmented two-kernel with the lane-local range decode (default),
-    1 = per-tile, 2 = warp-tile, 3 = warp-sliced v3, 4 = CTA-pipelined single
-    pass, 5 = segmented with the V/EP-window range decode.  Batched lists
-    follow 0 / 5."""
+    """Testing switch (internal symbol mvbx_set_kernel): strict-mode stream
+    decoder 0 = the single-read fused decoder (default), 1 = the per-tile
+    kernel (which serves permissive mode), 6 = the two-kernel segmented
+    decoder (whose launch pair the pipelined host drop-in uses).  Batched
+    lists have one kernel."""
     f = lib().mvbx_set_kernel
     f.argtypes = [ctypes.c_int]
     f.restype = None

@@ -460,9 +460,6 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
             F5 &= T32;
         }
         if (n_w) last_i = i;
-#if MVB_PATH_STATS
-        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : (takef || takef5) ? 1 : inter ? 2 : 3], 1ull);
-#endif
         if (take3) {
             // carry: complete integers before the slice -> every byte before it
             const uint32_t hin = __shfl_sync(0xFFFFFFFFu, tail_value(wp3), 0);

@@ -31,26 +31,15 @@
 // see them and combined by the last CTA.
 #pragma once
 
-#include "decode_pipelined.cuh"
+#include "decode_kernel.cuh"
 #include "totals_kernel.cuh"
 
 namespace mvbk {
 
-#ifndef MVB_TRACE_B
-#define MVB_TRACE_B 0  // 1: kernel B records per-warp timestamps (profiling builds only)
-#endif
-#if MVB_TRACE_B
-__device__ unsigned long long* mvb_trace_b;  // 6 words per warp: start, after wait, after prefix, end, segments, SM
-#endif
 
 constexpr int kSegWarps = 4;  // warps per CTA
 constexpr int kSegThreads = 32 * kSegWarps;
 constexpr int kSegSlice = 512;
-constexpr int kSegGroup = 2;  // slices scanned before one phase 2 (fills its passes: ~341 ints/slice on c2)
-constexpr int kSegVW = 8 + kSegGroup * 512 + 8;   // V words per warp: 8 halo + the group's positions + pad (64-B multiple)
-constexpr int kSegEPH = 8 + kSegGroup * 512 + 8;  // EP halfwords per warp: [7] previous end, [8 + k] ends, padding
-constexpr int kSegSmem = kSegWarps * (4 * kSegVW + 2 * kSegEPH);
-static_assert((4 * kSegVW) % 64 == 0 && (2 * kSegEPH) % 16 == 0, "alignment");
 
 struct SegParams {
     const uint8_t* in;  // stream start
@@ -528,204 +517,6 @@ struct RangeOut {
     unsigned long long n;
 };
 
-// One warp decodes the integers ending in slices [qs, qe) (512-byte steps,
-// qs 16-byte aligned) of range R: terminator scan, V digit windows and EP
-// end list in warp-private shared memory for kSegGroup slices at a time, then
-// one phase 2 over the group's integers (8 per lane per pass: two slices'
-// ~682 integers of c2 fill three passes to 89% instead of two to 67%),
-// in-warp delta prefix from `carry`, and 16-byte-aligned stores to
-// out[base ...] of every integer with output index < limit.
-template <bool kDelta>
-__device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, long long qe, unsigned long long base,
-                                             uint32_t carry, unsigned long long limit, uint32_t* out, char* vbase,
-                                             uint16_t* eph, int lane, const RangeSink& K, RangeOut& ro) {
-    const uint32_t r0 = 8u + 16u * static_cast<uint32_t>(lane);  // V index of this lane's chunk
-    const uintptr_t out_w = reinterpret_cast<uintptr_t>(out) >> 2;
-    unsigned long long run = base;  // output index of the next integer
-    long long last_end = -1;
-    uint32_t pw2 = 0, pw3 = 0;
-    if (lane == 0) {
-        if (r_inside(R, qs - 8, 8)) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(R.ab + qs - 8));
-            pw2 = v.x;
-            pw3 = v.y;
-        } else {
-            pw2 = r_word(R, qs - 8);
-            pw3 = r_word(R, qs - 4);
-        }
-    }
-    uint4 nx = r_load16(R, qs + 16 * lane);  // prefetched slice
-    for (long long qg = qs; qg < qe; qg += kSegGroup * kSegSlice) {
-        // ---- scan up to kSegGroup slices into one V / EP window ----
-        uint32_t n_g = 0;  // integers of the group so far (warp-uniform)
-#pragma unroll 1
-        for (int h = 0; h < kSegGroup; ++h) {
-            const long long q = qg + h * kSegSlice;
-            if (q >= qe) break;
-            const long long q0 = q + 16 * lane;
-            const uint4 x = nx;
-            if (q + kSegSlice < qe) nx = r_load16(R, q0 + kSegSlice);
-            const uint32_t w0 = x.x, w1 = x.y, w2 = x.z, w3 = x.w;
-            uint32_t wp2 = __shfl_up_sync(0xFFFFFFFFu, w2, 1), wp3 = __shfl_up_sync(0xFFFFFFFFu, w3, 1);
-            uint32_t wn = __shfl_down_sync(0xFFFFFFFFu, w0, 1);
-            const uint32_t l2 = __shfl_sync(0xFFFFFFFFu, w2, 31), l3 = __shfl_sync(0xFFFFFFFFu, w3, 31);
-            const uint32_t nf = __shfl_sync(0xFFFFFFFFu, nx.x, 0);  // first word of the next slice
-            if (lane == 0) {
-                wp2 = pw2;
-                wp3 = pw3;
-            }
-            if (lane == 31)
-                wn = (q + kSegSlice < qe) ? nf
-                     : r_inside(R, q0 + 16, 4) ? __ldg(reinterpret_cast<const uint32_t*>(R.ab + q0 + 16))
-                                               : r_word(R, q0 + 16);
-            pw2 = l2;
-            pw3 = l3;
-
-            // ---- phase 1: terminators, counts ----
-            const uint32_t T16 = hibits16(~w0, ~w1, ~w2, ~w3);
-            const uint32_t Tx = (hibits4(~wp2) | (hibits4(~wp3) << 4)) | (T16 << 8) | (hibits4(~wn) << 24);
-            const uint32_t Cx = ~Tx & 0x0FFFFFFFu;
-            const uint32_t inr16 = r_inr16(R, q0);
-            const uint32_t ends16 = T16 & inr16;
-            const uint32_t n_own = __popc(ends16);
-            uint32_t incl = n_own;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            const uint32_t wexcl = incl - n_own;
-            const unsigned long long rs = run + n_g;  // output index of the slice's first integer
-            // strict: a fifth byte >= 0x10 (4 continuation bytes after an integer end)
-            uint32_t bad16 = 0;
-            if (Cx & (Cx >> 1) & (Cx >> 2) & (Cx >> 3)) {
-                const uint32_t five = (Tx >> 3) & (Cx >> 4) & (Cx >> 5) & (Cx >> 6) & (Cx >> 7) & inr16;
-                if (five) {
-                    const uint32_t g0 = w0 | (w0 << 1) | (w0 << 2) | (w0 << 3);
-                    const uint32_t g1 = w1 | (w1 << 1) | (w1 << 2) | (w1 << 3);
-                    const uint32_t g2 = w2 | (w2 << 1) | (w2 << 2) | (w2 << 3);
-                    const uint32_t g3 = w3 | (w3 << 1) | (w3 << 2) | (w3 << 3);
-                    bad16 = five & hibits16(g0, g1, g2, g3);
-                }
-            }
-            if (__any_sync(0xFFFFFFFFu, bad16)) {  // rare: the slice's first malformed integer
-                const int j = bad16 ? __ffs(bad16) - 1 : 0;
-                unsigned long long idx = bad16 ? rs + wexcl + __popc(ends16 & ((1u << j) - 1u)) : ~0ull;
-                long long pos = q0 + j - 4 - R.lo;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
-                    const long long op = __shfl_xor_sync(0xFFFFFFFFu, pos, o);
-                    if (oi < idx) {
-                        idx = oi;
-                        pos = op;
-                    }
-                }
-                if (lane == 0) sink_error(K, idx, pos, limit);
-            }
-            if (n_w == 0) continue;  // warp-uniform (the next slice writes its own halo V)
-            // end of integer limit-1, if it ends in this slice
-            if (limit - rs <= n_w && limit - 1 - rs >= wexcl && limit - 1 - rs < wexcl + n_own) {
-                uint32_t m = ends16;
-                for (unsigned r = static_cast<unsigned>(limit - 1 - rs - wexcl); r > 0; --r) m &= m - 1;
-                sink_count_end(K, q0 + (__ffs(m) - 1) + 1 - R.lo);
-            }
-            if (wexcl + n_own == n_w && n_own) last_end = q0 + (31 - __clz(ends16)) + 1 - R.lo;
-
-            // ---- V digit windows and EP ends (V index = 8 + 512h + slice position) ----
-            const uint32_t rh = r0 + 512u * h;
-            const uint32_t d0 = digits4(w0), d1 = digits4(w1), d2 = digits4(w2), d3 = digits4(w3), dn = digits4(wn);
-            const uint32_t vo = 4u * rh;
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo)) = vquad(d0, d1);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 16)) = vquad(d1, d2);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 32)) = vquad(d2, d3);
-            *reinterpret_cast<uint4*>(vbase + v_swz(vo + 48)) = vquad(d3, dn);
-            if (lane == 0) {
-                const uint32_t dp2 = digits4(wp2), dp3 = digits4(wp3);
-                *reinterpret_cast<uint4*>(vbase + v_swz(2048u * h)) = vquad(dp2, dp3);
-                *reinterpret_cast<uint4*>(vbase + v_swz(2048u * h + 16)) = vquad(dp3, d0);
-                if (n_g == 0) {  // the group's first integer: its predecessor's end (V index)
-                    const uint32_t tp8 = Tx & 0xFFu;  // positions -8..-1
-                    // the range start is an integer boundary: the padding before it
-                    // holds no integers (they are masked out of ends16)
-                    eph[7] = (q <= R.lo) ? static_cast<uint16_t>(512u * h + 7 + (R.lo - q))
-                             : static_cast<uint16_t>(tp8 ? 512u * h + (31 - __clz(tp8)) : (512u * h - 1u) & 0xFFFFu);
-                }
-            }
-            uint16_t* ep = eph + 8 + n_g + wexcl;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if ((ends16 >> j) & 1u) {
-                    *ep = static_cast<uint16_t>(rh + j);
-                    ++ep;
-                }
-            }
-            if (n_own && wexcl + n_own == n_w) {  // zero-width padding for the last octet
-                const uint16_t rl = static_cast<uint16_t>(rh + (31 - __clz(ends16)));
-#pragma unroll
-                for (int k = 0; k < 8; ++k) ep[k] = rl;
-            }
-            n_g += n_w;
-        }
-        if (n_g == 0) continue;
-        __syncwarp();
-
-        // ---- phase 2 and stores: 8 integers per lane per pass ----
-        for (uint32_t q2 = 0; q2 < n_g; q2 += 256) {
-            const uint32_t u = q2 + 8u * lane;
-            uint32_t val[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) val[k] = 0;
-            if (u < n_g) {
-                const uint4 ea = *reinterpret_cast<const uint4*>(eph + 8 + u);  // 8 ends
-                const uint32_t e[9] = {eph[7 + u], ea.x & 0xFFFFu, ea.x >> 16, ea.y & 0xFFFFu, ea.y >> 16,
-                                       ea.z & 0xFFFFu, ea.z >> 16, ea.w & 0xFFFFu, ea.w >> 16};
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    val[k] = *reinterpret_cast<const uint32_t*>(vbase + v_swz(4u * ((e[k] + 1u) & 0xFFFFu))) &
-                             bmsk(7u * ((e[k + 1] - e[k]) & 0xFFFFu));
-            }
-            if (kDelta) {
-#pragma unroll
-                for (int k = 1; k < 8; ++k) val[k] += val[k - 1];
-                uint32_t xs = val[7];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xs, o);
-                    if (lane >= o) xs += y;
-                }
-                const uint32_t ex = carry + xs - val[7];
-                carry += __shfl_sync(0xFFFFFFFFu, xs, 31);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) val[k] += ex;
-            }
-            const unsigned long long gi = run + q2;  // output index of this pass's first integer
-            if (gi < limit) {
-                const unsigned long long room = limit - gi;
-                const unsigned npass = n_g - q2 < 256u ? n_g - q2 : 256u;
-                const unsigned plim = room < npass ? static_cast<unsigned>(room) : npass;
-                uint32_t* const op = out + gi;
-                switch ((4u - static_cast<unsigned>((out_w + gi) & 3u)) & 3u) {
-                    case 0: store_octets<0>(op, val, lane, plim); break;
-                    case 1: store_octets<1>(op, val, lane, plim); break;
-                    case 2: store_octets<2>(op, val, lane, plim); break;
-                    default: store_octets<3>(op, val, lane, plim); break;
-                }
-            }
-        }
-        run += n_g;
-        __syncwarp();  // V / EP are rewritten by the next group
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const long long le = __shfl_xor_sync(0xFFFFFFFFu, last_end, o);
-        last_end = le > last_end ? le : last_end;
-    }
-    ro.last_end = last_end;
-    ro.n = run - base;
-}
-
 // ------------------------------------------------------------------ lane-local range decode
 
 // The same contract as decode_range, computed the other way round: every lane
@@ -750,12 +541,6 @@ __device__ __forceinline__ void decode_range(const ByteRange& R, long long qs, l
 // integers, the end of integer limit-1).  Delta: in-lane running sums stay in
 // registers, the warp scan of the lane totals adds the offsets before the
 // stores.
-#ifndef MVB_PATH_STATS
-#define MVB_PATH_STATS 0  // (profiling builds: count 32-byte-lane slices per path)
-#endif
-#if MVB_PATH_STATS
-__device__ unsigned long long mvb_path_counts[4];  // 2-byte, fast, general interior, general edge
-#endif
 #ifndef MVB_FAST5
 #define MVB_FAST5 1  // plain slices with canonical 5-byte integers on the fast path
 #endif
@@ -1593,9 +1378,6 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
             F5 &= T32;
         }
         if (n_w) last_i = i;
-#if MVB_PATH_STATS
-        if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : (takef || takef5) ? 1 : inter ? 2 : 3], 1ull);
-#endif
         if (take2 || takef || takef5) {
             if (take2)
                 lane_slots_2b<kDelta, kSwz, 8>(wp3, w, T32 & inr32, st_base + 4u * (a + wexcl), carry);
@@ -1726,9 +1508,6 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
             const bool take2 = (inter || tail || MVB_HEAD2) && vote == 0;  // (head slices: see decode_range_ll)
             const bool takef = !take2 && inter && !(vote & 2u);
             if (n_w) last_i = i;
-#if MVB_PATH_STATS
-            if (lane == 0) atomicAdd(&mvb_path_counts[take2 ? 0 : takef ? 1 : inter ? 2 : 3], 1ull);
-#endif
             if (take2 || takef) {
                 if (take2) {
                     const uint32_t wv[4] = {w0, w1, w2, w3};
@@ -1974,42 +1753,33 @@ __device__ __forceinline__ void seg_prefix(const SegParams& S, long long s, int 
     }
 }
 
-// kLL: 0 decode_range (V / EP windows), 1 decode_range_ll (lane-local)
-template <bool kDelta, int kLL>
-__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 8) vbyte_seg_decode(SegParams S) {
+template <bool kDelta>
+__global__ void __launch_bounds__(kSegThreads, kDelta ? kLLBlocksD : kLLBlocks) vbyte_seg_decode(SegParams S) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
-    uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * kLaneWarpBytes;
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
-    // kLL: one contiguous run of segments per warp (the output index and carry
-    // after segment s are those of s + 1, so only the run's first segment needs
-    // the prefix); otherwise segments round-robin.
+    // one contiguous run of segments per warp (the output index and carry after
+    // segment s are those of s + 1, so only the run's first segment needs the
+    // prefix)
     const long long ns = S.s_hi - S.s_lo;
-    const long long s0 = S.s_lo + (kLL ? gw * ns / nw : gw), s_step = kLL ? ns : nw;
-    const long long s0_end = kLL ? S.s_lo + (gw + 1) * ns / nw : 0;  // balanced runs: sizes differ by at most one
+    const long long s0 = S.s_lo + gw * ns / nw, s_step = ns;
+    const long long s0_end = S.s_lo + (gw + 1) * ns / nw;  // balanced runs: sizes differ by at most one
     // kernel A's totals are complete and visible after this (a no-op unless
     // launched as a programmatic dependent)
-#if MVB_TRACE_B
-    unsigned long long t_trace[4];
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[0]));
-#endif
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #if MVB_A_PDL
     // the next decode's kernel A may start its loads as this grid's CTAs retire
     // (it waits for this grid before its first write)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
-#if MVB_TRACE_B
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[1]));
-#endif
 
-    for (long long s = s0; s < (kLL ? s0_end : S.s_hi); s += s_step) {
-        const long long s_end = kLL ? s0_end : s + 1;
+    for (long long s = s0; s < s0_end; s += s_step) {
+        const long long s_end = s0_end;
         // ---- output index and carry of the segment ----
         unsigned long long base, csum;
         seg_prefix<kDelta>(S, s, lane, base, csum);
@@ -2027,11 +1797,8 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
             kDelta ? static_cast<uint32_t>(csum) - straddle + (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
         RangeOut ro;
         const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
-#if MVB_TRACE_B
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[2]));
-#endif
-        if (kLL) {
-            // integers in the run (segments s .. s_end - 1, at most 32 when kLL): its density
+        {
+            // integers in the run (segments s .. s_end - 1, at most 32): its density
             unsigned long long rc = (s + lane < s_end) ? S.scnt[s + lane] : 0u;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(0xFFFFFFFFu, rc, o);
@@ -2046,29 +1813,10 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
                 decode_range_llw<kDelta, false>(R, s * S.seg_bytes, qe, base, carry, S.count, S.out,
                                                reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
         }
-        else
-            decode_range<kDelta>(R, s * S.seg_bytes, (s + 1) * S.seg_bytes, base, carry, S.count, S.out, vbase, eph,
-                                 lane, K, ro);
-        if (!kLL && lane == 0 && ro.last_end >= 0)
-            atomicMax(&S.hdr->last_end, static_cast<unsigned long long>(ro.last_end));
     }
-#if MVB_TRACE_B
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_trace[3]));
-    if (lane == 0 && mvb_trace_b) {
-        unsigned long long* t = mvb_trace_b + 6 * gw;
-        t[0] = t_trace[0];
-        t[1] = t_trace[1];
-        t[2] = t_trace[2];
-        t[3] = t_trace[3];
-        t[4] = static_cast<unsigned long long>(s0_end - s0);
-        unsigned smid;
-        asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        t[5] = smid;
-    }
-#endif
 
     // ---- completion; the last CTA produces the DecodeResult ----
-    seg_complete<kSegWarps>(S, kLL != 0);
+    seg_complete<kSegWarps>(S, true);
 }
 
 // ------------------------------------------------------------------ batched lists
@@ -2094,16 +1842,15 @@ struct ListParams {
     WsHeader* hdr;
 };
 
-template <bool kDelta, int kLL>
-__global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLBlocks) : 1) vbyte_lists_decode(ListParams L) {
+template <bool kDelta>
+__global__ void __launch_bounds__(kSegThreads, kDelta ? kLLBlocksD : kLLBlocks) vbyte_lists_decode(ListParams L) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ bool s_last;
     __shared__ unsigned long long s_err_idx[kSegWarps];
     __shared__ long long s_err_pos[kSegWarps], s_count_end[kSegWarps];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    char* const vbase = reinterpret_cast<char*>(smem) + wid * (kLL ? kLaneWarpBytes : 4 * kSegVW);
-    uint16_t* const eph = reinterpret_cast<uint16_t*>(smem + kSegWarps * 4 * kSegVW) + wid * kSegEPH;
+    char* const vbase = reinterpret_cast<char*>(smem) + wid * kLaneWarpBytes;
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
     while (true) {
         long long k = 0;
@@ -2132,15 +1879,13 @@ __global__ void __launch_bounds__(kSegThreads, kLL ? (kDelta ? kLLBlocksD : kLLB
             RangeOut ro;
             const RangeSink K = {nullptr, &s_err_idx[wid], &s_err_pos[wid], &s_count_end[wid]};
             const uint32_t carry = kDelta && L.prev ? L.prev[l] : 0u;
-            if (kLL)
-                if (range_dense(cnt, R.hi - R.lo))
+            if (range_dense(cnt, R.hi - R.lo))
                     decode_range_llw<kDelta, true>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
                                                   reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
                 else
                     decode_range_llw<kDelta, false>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out,
                                                    reinterpret_cast<uint32_t*>(vbase), ring, lane, K, ro);
-            else
-                decode_range<kDelta>(R, R.lo & ~15ll, R.hi, base, carry, base + cnt, L.out, vbase, eph, lane, K, ro);
+
             __syncwarp();
             const unsigned long long ei = s_err_idx[wid];
             if (ei != ~0ull && ei < base + cnt) {

@@ -16,11 +16,8 @@
 
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
-#include "decode_pipelined.cuh"
-#include "decode_v3.cuh"
 #include "decode_seg.cuh"
 #include "decode_fused.cuh"
-#include "decode_warp.cuh"
 #include "totals_kernel.cuh"
 #include "encode_kernel.cuh"
 
@@ -44,14 +41,6 @@ size_t groups_for(size_t tiles) { return (tiles + mvbk::kGroup - 1) / mvbk::kGro
 // Workspace bytes for a launch of `tiles` tiles (layout in decode_kernel.cuh).
 size_t ws_need(size_t tiles) {
     return kHeaderBytes + (tiles * mvbk::kDescArrays + groups_for(tiles) * mvbk::kGroupArrays) * 8;
-}
-
-// Warp-tile kernel (decode_warp.cuh): header | count[n] | sum[n] | group count/sum [ng] x2 |
-// supergroup count/sum [ns] x2 | group accumulators [ng] x2 | supergroup accumulators [ns] x2.
-size_t wtiles_for(size_t mis, size_t scan_len) { return (mis + scan_len + mvbk::kWTile - 1) / mvbk::kWTile; }
-size_t ws_need_warp(size_t wtiles) {
-    const size_t ng = (wtiles + 31) / 32, ns = (ng + 31) / 32;
-    return kHeaderBytes + (2 * wtiles + 4 * ng + 4 * ns) * 8;
 }
 
 // Bytes the decode of `count` integers can touch: every integer (strict or
@@ -81,46 +70,41 @@ size_t scan_length(size_t in_len, size_t count) {
     return std::min(in_len, count * 5);
 }
 
-// Strict-mode kernel: 0 segmented two-kernel decode with the lane-local range
-// decode (default, decode_seg.cuh: decode_range_ll), 1 per-tile kernel, 2
-// warp-tile kernel, 3 warp-sliced v3 (decode_v3.cuh), 4 CTA-pipelined single
-// pass (decode_pipelined.cuh; also the traced kernel), 5 segmented with the
-// V/EP-window range decode (decode_range).  Batched lists follow 0 / 5.
-// Permissive mode always runs the per-tile kernel (it needs a third lookback
-// component inside phase 1).  The switch exists for profiling comparisons.
+// Strict-mode kernel: 0 the single-read fused decoder (default,
+// decode_fused.cuh); 1 the per-tile kernel (decode_kernel.cuh, which serves
+// permissive mode); 6 the two-kernel segmented decoder (decode_seg.cuh; the
+// pipelined host drop-in's chunks use its launch pair).  Internal switch for
+// tests and comparisons (mvbx_set_kernel), not part of the C ABI.
 int g_kernel_choice = 0;
+
+// Occupancy of a kernel on the current device (cached per kernel and device).
+int occupancy(const void* fn, int threads, size_t smem, int* sms_out) {
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    *sms_out = sms;
+    const unsigned long long key = (reinterpret_cast<uintptr_t>(fn) << 8) ^ static_cast<unsigned long long>(dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return -1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return -1;
+    if (n < 1) n = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = n;
+    return n;
+}
 
 template <bool Delta, int Mode>
 cudaError_t launch(const Params& p, cudaStream_t s) {
     mvbk::vbyte_decode_kernel<Delta, Mode><<<p.n_tiles, mvbk::kThreads, 0, s>>>(p);
-    return cudaGetLastError();
-}
-
-// Persistent launch: as many CTAs as can be co-resident (the lookback of a
-// tile may wait on any earlier tile, so every CTA must be running), capped by
-// the number of tiles.
-template <bool Delta, bool Trace>
-cudaError_t launch_pipelined_t(const Params& p, cudaStream_t s) {
-    static int per_sm = -1;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    int sms = 0;
-    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 0) {
-        e = cudaFuncSetAttribute(mvbk::vbyte_decode_pipelined<Delta, Trace>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mvbk::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        int n = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_pipelined<Delta, Trace>,
-                                                          mvbk::kPThreads, mvbk::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        per_sm = n > 0 ? n : 1;
-    }
-    const long long cap = static_cast<long long>(per_sm) * sms;
-    const unsigned grid = static_cast<unsigned>(p.n_tiles < cap ? p.n_tiles : cap);
-    mvbk::vbyte_decode_pipelined<Delta, Trace><<<grid, mvbk::kPThreads, mvbk::kSmemBytes, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -137,45 +121,17 @@ struct SegLaunch {
     unsigned grid_a_cap, grid_b_cap, grid_a_launch;
 };
 
-// LL: 0 V/EP range decode (choice 5), 1 lane-local (choice 0, default).
-template <int LL>
-constexpr int seg_b_smem() { return LL ? mvbk::kLaneSmem : mvbk::kSegSmem; }
-template <int LL>
-constexpr int seg_b_threads() { return mvbk::kSegThreads; }
-template <bool Delta, int LL>
-constexpr auto seg_b_kernel() { return mvbk::vbyte_seg_decode<Delta, LL>; }
 
-template <bool Delta, int LL>
+template <bool Delta>
 int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cudaStream_t s, SegLaunch& sl) {
-    constexpr int kSmemB = seg_b_smem<LL>();
-    static int per_sm = -1;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return MVB_ERR_CUDA;
     int sms = 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return MVB_ERR_CUDA;
-    if (per_sm < 0) {
-        if (cudaFuncSetAttribute(seg_b_kernel<Delta, LL>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemB) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, seg_b_kernel<Delta, LL>(), seg_b_threads<LL>(),
-                                                          kSmemB) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        per_sm = n > 0 ? n : 1;
-    }
-    static int per_sm_a = -1;
-    if (per_sm_a < 0) {
-        int n = 0;
-        if (cudaFuncSetAttribute(mvbk::vbyte_seg_totals<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kASmem) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_seg_totals<Delta>, mvbk::kSegThreads,
-                                                          mvbk::kASmem) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        per_sm_a = n > 0 ? n : 1;
-    }
+    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_seg_decode<Delta>), mvbk::kSegThreads,
+                                 mvbk::kLaneSmem, &sms);
+    const int per_sm_a = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_seg_totals<Delta>), mvbk::kSegThreads,
+                                   mvbk::kASmem, &sms);
+    if (per_sm < 0 || per_sm_a < 0) return MVB_ERR_CUDA;
     const long long ctas = static_cast<long long>(per_sm) * sms;
-    const long long warps = ctas * (seg_b_threads<LL>() / 32);
+    const long long warps = ctas * (mvbk::kSegThreads / 32);
     const long long qlen = p.mis + p.len;
     // segments per kernel-B warp: LL decodes a balanced contiguous run of them per
     // warp (finer is better balanced), V/EP hands them out round-robin
@@ -183,7 +139,7 @@ int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cu
     // (about 32 segments per warp: 1 KiB on c2), V/EP hands them out round-robin
     long long seg;
     {
-        const long long per_warp = LL ? 1 : 4;  // LL: one segment (a balanced byte range) per warp
+        const long long per_warp = 1;  // one segment (a balanced byte range) per warp
         seg = (plan_len + per_warp * warps - 1) / (per_warp * warps);
         seg = (seg + mvbk::kSegASlice - 1) / mvbk::kSegASlice * mvbk::kSegASlice;  // kernel A: whole iterations
         if (seg < mvbk::kSegASlice) seg = mvbk::kSegASlice;
@@ -228,11 +184,11 @@ int seg_setup(const Params& p, void* ws, size_t ws_bytes, long long plan_len, cu
     return 0;
 }
 
-template <bool Delta, int LL>
+template <bool Delta>
 int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_launch,
                     volatile unsigned long long* chunk_total, const unsigned long long* base_in,
                     unsigned long long* base_out, cudaStream_t s) {
-    constexpr int kSmemB = seg_b_smem<LL>();
+    constexpr int kSmemB = mvbk::kLaneSmem;
     mvbk::SegParams S = sl.S;
     S.s_lo = s_lo;
     S.s_hi = s_hi;
@@ -290,7 +246,7 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     // results in griddepcontrol.wait (hides B's launch latency behind A's tail)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid_b);
-    cfg.blockDim = dim3(seg_b_threads<LL>());
+    cfg.blockDim = dim3(mvbk::kSegThreads);
     cfg.dynamicSmemBytes = kSmemB;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -298,41 +254,16 @@ int seg_launch_pair(SegLaunch& sl, long long s_lo, long long s_hi, bool final_la
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, seg_b_kernel<Delta, LL>(), S) != cudaSuccess) return MVB_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_seg_decode<Delta>, S) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
-template <bool Delta, int LL>
+template <bool Delta>
 int launch_seg(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     SegLaunch sl;
-    const int rc = seg_setup<Delta, LL>(p, ws, ws_bytes, p.mis + p.len, s, sl);
+    const int rc = seg_setup<Delta>(p, ws, ws_bytes, p.mis + p.len, s, sl);
     if (rc) return rc;
-    return seg_launch_pair<Delta, LL>(sl, 0, sl.S.n_seg, true, nullptr, nullptr, nullptr, s);
-}
-
-// Occupancy of a kernel on the current device (cached per kernel and device).
-int occupancy(const void* fn, int threads, size_t smem, int* sms_out) {
-    static std::mutex mu;
-    static std::unordered_map<unsigned long long, int> cache;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
-    int sms = 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
-    *sms_out = sms;
-    const unsigned long long key = (reinterpret_cast<uintptr_t>(fn) << 8) ^ static_cast<unsigned long long>(dev);
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) return it->second;
-    }
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
-        return -1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return -1;
-    if (n < 1) n = 1;
-    std::lock_guard<std::mutex> lk(mu);
-    cache[key] = n;
-    return n;
+    return seg_launch_pair<Delta>(sl, 0, sl.S.n_seg, true, nullptr, nullptr, nullptr, s);
 }
 
 // Single-read strict decode (decode_fused.cuh): one persistent launch over
@@ -419,68 +350,9 @@ int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 
-// Persistent warp-sliced launch (decode_v3.cuh).
-template <bool Delta>
-cudaError_t launch_v3(const mvbk::WParams& p, cudaStream_t s) {
-    static int per_sm = -1;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    int sms = 0;
-    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 0) {
-        e = cudaFuncSetAttribute(mvbk::vbyte_decode_v3<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kS3Bytes);
-        if (e != cudaSuccess) return e;
-        int n = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_v3<Delta>, mvbk::kV3Threads,
-                                                          mvbk::kS3Bytes);
-        if (e != cudaSuccess) return e;
-        per_sm = n > 0 ? n : 1;
-    }
-    const long long cap = static_cast<long long>(per_sm) * sms;
-    const unsigned grid = static_cast<unsigned>(p.p.n_tiles < cap ? p.p.n_tiles : cap);
-    mvbk::vbyte_decode_v3<Delta><<<grid, mvbk::kV3Threads, mvbk::kS3Bytes, s>>>(p);
-    return cudaGetLastError();
-}
-
-template <bool Delta>
-cudaError_t launch_warp(const mvbk::WParams& w, unsigned n_wtiles, cudaStream_t s) {
-    static int per_sm = -1;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    int sms = 0;
-    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 0) {
-        e = cudaFuncSetAttribute(mvbk::vbyte_decode_warp<Delta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 mvbk::kWSmemBytes);
-        if (e != cudaSuccess) return e;
-        int n = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_decode_warp<Delta>, mvbk::kWThreads,
-                                                          mvbk::kWSmemBytes);
-        if (e != cudaSuccess) return e;
-        per_sm = n > 0 ? n : 1;
-    }
-    // every warp must be resident (a lookback may wait on any earlier tile)
-    const long long cap = static_cast<long long>(per_sm) * sms;
-    const long long need = (static_cast<long long>(n_wtiles) + mvbk::kWWarps - 1) / mvbk::kWWarps;
-    const unsigned grid = static_cast<unsigned>(need < cap ? need : cap);
-    mvbk::vbyte_decode_warp<Delta><<<grid, mvbk::kWThreads, mvbk::kWSmemBytes, s>>>(w);
-    return cudaGetLastError();
-}
-
-template <bool Delta>
-cudaError_t launch_pipelined(const Params& p, cudaStream_t s) {
-    return p.trace ? launch_pipelined_t<Delta, true>(p, s) : launch_pipelined_t<Delta, false>(p, s);
-}
-
 int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
                   uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
-                  cudaStream_t stream, unsigned long long* trace = nullptr,
-                  const uint32_t* prev_dev = nullptr) {
+                  cudaStream_t stream, const uint32_t* prev_dev = nullptr) {
     if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
     if (mode != MVB_STRICT && mode != MVB_PERMISSIVE) return MVB_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
@@ -495,12 +367,8 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
     const size_t scan = scan_length(in_len, count);
     const size_t tiles = tiles_for(mis, scan);
-    const bool warp_kernel = mode == MVB_STRICT && g_kernel_choice == 2 && trace == nullptr;
-    const bool v3_kernel = mode == MVB_STRICT && g_kernel_choice == 3;
-    const size_t wtiles = wtiles_for(mis, scan);
-    const size_t need = warp_kernel ? ws_need_warp(wtiles) : v3_kernel ? ws_need_warp(tiles) : ws_need(tiles);
-    if (ws == nullptr || ws_bytes < need) return MVB_ERR_WORKSPACE;
-    if (wtiles >= (1ull << 40)) return MVB_ERR_INVALID_ARG;
+    if (scan >= (1ull << 40)) return MVB_ERR_INVALID_ARG;
+    if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
 
     Params p;
     p.in = in;
@@ -512,6 +380,16 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.prev_dev = prev_dev;
     p.n_tiles = static_cast<unsigned>(tiles);
     p.hdr = static_cast<WsHeader*>(ws);
+    p.res_dev = res_dev;
+    p.trace = nullptr;
+
+    if (mode == MVB_STRICT && g_kernel_choice == 0)
+        return delta ? launch_fused<true>(p, ws, ws_bytes, stream) : launch_fused<false>(p, ws, ws_bytes, stream);
+    if (mode == MVB_STRICT && g_kernel_choice == 6)
+        return delta ? launch_seg<true>(p, ws, ws_bytes, stream) : launch_seg<false>(p, ws, ws_bytes, stream);
+    // per-tile kernel: permissive mode (and strict choice 1)
+    const size_t need = ws_need(tiles);
+    if (ws_bytes < need) return MVB_ERR_WORKSPACE;
     p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
     p.dsum = p.dcnt + tiles;
     p.dmax = p.dsum + tiles;
@@ -520,61 +398,9 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     p.gsum = p.gcnt + p.n_groups;
     p.gacc_cnt = p.gsum + p.n_groups;
     p.gacc_sum = p.gacc_cnt + p.n_groups;
-    p.res_dev = res_dev;
-    p.trace = trace;
-
-    if (mode == MVB_STRICT && g_kernel_choice == 0 && trace == nullptr)
-        return delta ? launch_fused<true>(p, ws, ws_bytes, stream) : launch_fused<false>(p, ws, ws_bytes, stream);
-    if (mode == MVB_STRICT && g_kernel_choice == 6 && trace == nullptr)
-        return delta ? launch_seg<true, 1>(p, ws, ws_bytes, stream) : launch_seg<false, 1>(p, ws, ws_bytes, stream);
-    if (mode == MVB_STRICT && g_kernel_choice == 5 && trace == nullptr)
-        return delta ? launch_seg<true, 0>(p, ws, ws_bytes, stream) : launch_seg<false, 0>(p, ws, ws_bytes, stream);
-    {
-        const unsigned long long family = warp_kernel ? 2 : v3_kernel ? 3 : 1;
-        const unsigned long long units = warp_kernel ? wtiles : tiles;
-        if (prepare_workspace(ws, need, (family << 56) | units, stream) != cudaSuccess) return MVB_ERR_CUDA;
-    }
+    if (prepare_workspace(ws, need, (1ull << 56) | tiles, stream) != cudaSuccess) return MVB_ERR_CUDA;
     cudaError_t e;
-    if (v3_kernel) {
-        // three-level descriptor layout of decode_warp.cuh, over 4 KiB tiles
-        mvbk::WParams w;
-        w.p = p;
-        const size_t ng = (tiles + 31) / 32, ns = (ng + 31) / 32;
-        w.n_groups = static_cast<long long>(ng);
-        w.n_super = static_cast<long long>(ns);
-        w.p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
-        w.p.dsum = w.p.dcnt + tiles;
-        w.g1cnt = w.p.dsum + tiles;
-        w.g1sum = w.g1cnt + ng;
-        w.g2cnt = w.g1sum + ng;
-        w.g2sum = w.g2cnt + ns;
-        w.a1cnt = w.g2sum + ns;
-        w.a1sum = w.a1cnt + ng;
-        w.a2cnt = w.a1sum + ng;
-        w.a2sum = w.a2cnt + ns;
-        e = delta ? launch_v3<true>(w, stream) : launch_v3<false>(w, stream);
-    } else if (warp_kernel) {
-        mvbk::WParams w;
-        w.p = p;
-        w.p.n_tiles = static_cast<unsigned>(wtiles);
-        const size_t ng = (wtiles + 31) / 32, ns = (ng + 31) / 32;
-        w.n_groups = static_cast<long long>(ng);
-        w.n_super = static_cast<long long>(ns);
-        w.p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
-        w.p.dsum = w.p.dcnt + wtiles;
-        w.g1cnt = w.p.dsum + wtiles;
-        w.g1sum = w.g1cnt + ng;
-        w.g2cnt = w.g1sum + ng;
-        w.g2sum = w.g2cnt + ns;
-        w.a1cnt = w.g2sum + ns;
-        w.a1sum = w.a1cnt + ng;
-        w.a2cnt = w.a1sum + ng;
-        w.a2sum = w.a2cnt + ns;
-        e = delta ? launch_warp<true>(w, static_cast<unsigned>(wtiles), stream)
-                  : launch_warp<false>(w, static_cast<unsigned>(wtiles), stream);
-    } else if (mode == MVB_STRICT && (g_kernel_choice == 4 || g_kernel_choice == 0 || trace != nullptr))
-        e = delta ? launch_pipelined<true>(p, stream) : launch_pipelined<false>(p, stream);
-    else if (delta)
+    if (delta)
         e = mode == MVB_STRICT ? launch<true, mvbk::MODE_STRICT>(p, stream)
                                : launch<true, mvbk::MODE_PERMISSIVE>(p, stream);
     else
@@ -638,17 +464,47 @@ struct HostCtx {
         ok = true;
         return true;
     }
+    // (zeroed on this context's own stream and waited for: the decode kernels
+    // run on non-blocking streams, which the legacy default stream does not
+    // order; the old buffer is freed only after this stream's earlier work)
     template <class T>
-    static bool grow(T*& p, size_t& cap, size_t need, bool zero) {
+    bool grow(T*& p, size_t& cap, size_t need, bool zero) {
         if (need <= cap) return true;
-        if (p) cudaFree(p);
+        if (p) {
+            if (cudaStreamSynchronize(stream) != cudaSuccess) return false;
+            cudaFree(p);
+        }
         p = nullptr;
         cap = 0;
         const size_t n = std::max<size_t>(need, 1u << 20);
         if (cudaMalloc(reinterpret_cast<void**>(&p), n) != cudaSuccess) return false;
-        if (zero && cudaMemset(p, 0, n) != cudaSuccess) return false;
+        if (zero && (cudaMemsetAsync(p, 0, n, stream) != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess))
+            return false;
         cap = n;
         return true;
+    }
+    // per-thread buffers go with the thread (errors ignored: at process exit
+    // the CUDA context may already be gone)
+    ~HostCtx() {
+        if (!ok) return;
+        cudaStreamSynchronize(stream);
+        cudaStreamSynchronize(d2h);
+        for (void* q : {static_cast<void*>(d_in), static_cast<void*>(d_out), d_ws, static_cast<void*>(d_res),
+                        static_cast<void*>(d_base), static_cast<void*>(d_bo), static_cast<void*>(d_io),
+                        static_cast<void*>(d_prev), static_cast<void*>(d_lres)})
+            if (q) cudaFree(q);
+        if (h_tot) cudaFreeHost(h_tot);
+        if (h_res) cudaFreeHost(h_res);
+        for (int i = 0; i < 64; ++i) {
+            cudaEventDestroy(ev_in[i]);
+            cudaEventDestroy(ev_kst[i]);
+            cudaEventDestroy(ev_dec[i]);
+            cudaEventDestroy(ev_out[i]);
+        }
+        cudaEventDestroy(ev_start);
+        cudaStreamDestroy(stream);
+        cudaStreamDestroy(h2d);
+        cudaStreamDestroy(d2h);
     }
 };
 
@@ -682,7 +538,7 @@ int decode_host_pipelined(HostCtx& c, const uint8_t* in, size_t scan, size_t cou
     // mapped host memory (a small D2H copy would queue behind the output copies)
     p.res_dev = c.dm_res;
     SegLaunch sl;
-    int rc = seg_setup<Delta, 1>(p, c.d_ws, c.ws_cap, static_cast<long long>(std::min(scan, g_pipe_chunk)), c.stream,
+    int rc = seg_setup<Delta>(p, c.d_ws, c.ws_cap, static_cast<long long>(std::min(scan, g_pipe_chunk)), c.stream,
                                  sl);
     if (rc) return rc;
     // chunk k covers segments [cb[k], cb[k + 1]): whole groups, the first of about
@@ -727,7 +583,7 @@ int decode_host_pipelined(HostCtx& c, const uint8_t* in, size_t scan, size_t cou
     auto kernels = [&](int k) -> int {
         if (cudaStreamWaitEvent(c.stream, c.ev_in[k], 0) != cudaSuccess) return MVB_ERR_CUDA;
         if (cudaEventRecord(c.ev_kst[k], c.stream) != cudaSuccess) return MVB_ERR_CUDA;
-        const int e = seg_launch_pair<Delta, 1>(sl, cb[k], cb[k + 1], k == n_chunks - 1, c.dm_tot + k,
+        const int e = seg_launch_pair<Delta>(sl, cb[k], cb[k + 1], k == n_chunks - 1, c.dm_tot + k,
                                                 k ? c.d_base + 2 * k : nullptr, c.d_base + 2 * (k + 1), c.stream);
         if (e) return e;
         if (k == n_chunks - 1 && k > 0) {  // segment totals are zero between decodes
@@ -774,12 +630,14 @@ int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint
     HostCtx& c = g_ctx;
     if (!c.init()) return MVB_ERR_CUDA;
     const size_t scan = scan_length(in_len, count);
+    // at most one integer per input byte can be decoded
+    const size_t n_out = std::min(count, scan);
     // the pipelined decode's segments can be finer than the one-shot decode's
     const size_t wsb = mvb_workspace_bytes(scan);
-    if (!HostCtx::grow(c.d_in, c.in_cap, scan, false) || !HostCtx::grow(c.d_out, c.out_cap, count * 4, false) ||
-        !HostCtx::grow(c.d_ws, c.ws_cap, wsb, true))
+    if (!c.grow(c.d_in, c.in_cap, scan, false) || !c.grow(c.d_out, c.out_cap, n_out * 4, false) ||
+        !c.grow(c.d_ws, c.ws_cap, wsb, true))
         return MVB_ERR_CUDA;
-    if (mode == MVB_STRICT && g_kernel_choice == 0 && count > 0 && scan >= g_pipe_min)
+    if (mode == MVB_STRICT && count > 0 && scan >= g_pipe_min)
         return delta ? decode_host_pipelined<true>(c, in, scan, count, prev, out, res)
                      : decode_host_pipelined<false>(c, in, scan, count, prev, out, res);
     if (scan && cudaMemcpyAsync(c.d_in, in, scan, cudaMemcpyHostToDevice, c.stream) != cudaSuccess)
@@ -787,11 +645,16 @@ int decode_host(const uint8_t* in, size_t in_len, size_t count, bool delta, uint
     const int rc = decode_device(scan ? c.d_in : nullptr, scan, count, delta, prev, count ? c.d_out : nullptr,
                                  mode, c.d_res, c.d_ws, c.ws_cap, c.stream);
     if (rc < 0) return rc;
+    // the result first, then exactly out[0 .. values_written): the rest of
+    // out is never touched (the device buffer may hold an earlier call's values)
     mvb_result r;
-    if (cudaMemcpyAsync(&r, c.d_res, sizeof r, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess) return MVB_ERR_CUDA;
-    if (count && cudaMemcpyAsync(out, c.d_out, count * 4, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess)
+    if (cudaMemcpyAsync(&r, c.d_res, sizeof r, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
+        cudaStreamSynchronize(c.stream) != cudaSuccess)
         return MVB_ERR_CUDA;
-    if (cudaStreamSynchronize(c.stream) != cudaSuccess) return MVB_ERR_CUDA;
+    const size_t n_copy = std::min<size_t>(static_cast<size_t>(r.values_written), n_out);
+    if (n_copy && (cudaMemcpyAsync(out, c.d_out, n_copy * 4, cudaMemcpyDeviceToHost, c.stream) != cudaSuccess ||
+                   cudaStreamSynchronize(c.stream) != cudaSuccess))
+        return MVB_ERR_CUDA;
     if (res) *res = r;
     return r.status;
 }
@@ -805,7 +668,7 @@ inline size_t vb_size(uint32_t x) {
 extern "C" {
 
 size_t mvb_workspace_bytes(size_t in_len) {
-    const size_t a = ws_need(tiles_for(15, in_len) + 1), b = ws_need_warp(wtiles_for(15, in_len) + 1);
+    const size_t a = ws_need(tiles_for(15, in_len) + 1), b = 0;
     // segmented decode with 1 KiB segments (the finest any launch uses)
     const size_t n_seg = (in_len + 15) / 1024 + 1, n_grp = n_seg / 32 + 1, n_sup = n_grp / 32 + 1;
     const size_t c = kHeaderBytes + 8 * n_seg + 16 * n_grp + 16 * n_sup;
@@ -839,7 +702,7 @@ int mvb_decode_delta_device_dprev(const uint8_t* in, size_t in_len, size_t count
                                   uint32_t* out, int mode, mvb_result* res_dev, void* ws, size_t ws_bytes,
                                   mvb_stream_t stream) {
     if (prev_dev == nullptr) return MVB_ERR_INVALID_ARG;
-    return decode_device(in, in_len, count, true, 0, out, mode, res_dev, ws, ws_bytes, stream, nullptr, prev_dev);
+    return decode_device(in, in_len, count, true, 0, out, mode, res_dev, ws, ws_bytes, stream, prev_dev);
 }
 
 int mvb_shard_carry_device(const unsigned long long* records, int n_ranks, int rank, int record_words,
@@ -855,8 +718,8 @@ int mvb_shard_carry_device(const unsigned long long* records, int n_ranks, int r
 }  // extern "C"
 
 namespace {
-template <bool Delta, int LL>
-int lists_device_t(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
+template <bool Delta>
+int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
                  const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, const unsigned* order,
                  uint32_t* out, int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n_lists == 0) return 0;
@@ -864,22 +727,11 @@ int lists_device_t(const uint8_t* in, size_t in_len, const unsigned long long* b
     if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;  // permissive lists: decode each list on its own
     if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
-    constexpr int kSmemB = LL ? mvbk::kLaneSmem : mvbk::kSegSmem;
-    static int per_sm = -1;
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        return MVB_ERR_CUDA;
-    if (per_sm < 0) {
-        if (cudaFuncSetAttribute(mvbk::vbyte_lists_decode<Delta, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemB) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mvbk::vbyte_lists_decode<Delta, LL>, mvbk::kSegThreads,
-                                                          kSmemB) != cudaSuccess)
-            return MVB_ERR_CUDA;
-        per_sm = n > 0 ? n : 1;
-    }
+    constexpr int kSmemB = mvbk::kLaneSmem;
+    int sms = 0;
+    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_lists_decode<Delta>), mvbk::kSegThreads,
+                                 kSmemB, &sms);
+    if (per_sm < 0) return MVB_ERR_CUDA;
     mvbk::ListParams L;
     const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
     L.ab = in - mis;
@@ -896,18 +748,8 @@ int lists_device_t(const uint8_t* in, size_t in_len, const unsigned long long* b
     const long long warps_needed = static_cast<long long>(n_lists);
     const long long ctas = std::min<long long>(static_cast<long long>(per_sm) * sms,
                                                (warps_needed + mvbk::kSegWarps - 1) / mvbk::kSegWarps);
-    mvbk::vbyte_lists_decode<Delta, LL><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
+    mvbk::vbyte_lists_decode<Delta><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
-}
-template <bool Delta>
-int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
-                 const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, const unsigned* order,
-                 uint32_t* out, int mode, mvb_result* results_dev, void* ws, size_t ws_bytes, cudaStream_t s) {
-    return g_kernel_choice == 5
-               ? lists_device_t<Delta, 0>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev,
-                                          ws, ws_bytes, s)
-               : lists_device_t<Delta, 1>(in, in_len, byte_off, int_off, prev, n_lists, order, out, mode, results_dev,
-                                          ws, ws_bytes, s);
 }
 // Batched host decode (mvb_decode_lists / mvb_decode_delta_lists): contiguous
 // sub-batches of lists, about g_pipe_chunk x 4 bytes or in_len / 16 each (at
@@ -926,13 +768,13 @@ int lists_host(const uint8_t* in, size_t in_len, const unsigned long long* byte_
     if (n_out > 0 && out == nullptr) return MVB_ERR_INVALID_ARG;
     HostCtx& c = g_ctx;
     if (!c.init()) return MVB_ERR_CUDA;
-    if (!HostCtx::grow(c.d_in, c.in_cap, in_len, false) ||
-        !HostCtx::grow(c.d_out, c.out_cap, static_cast<size_t>(n_out) * 4, false) ||
-        !HostCtx::grow(c.d_ws, c.ws_cap, mvb_workspace_bytes(0), true) ||
-        !HostCtx::grow(c.d_bo, c.bo_cap, (n_lists + 1) * 8, false) ||
-        !HostCtx::grow(c.d_io, c.io_cap, (n_lists + 1) * 8, false) ||
-        !HostCtx::grow(c.d_lres, c.lres_cap, n_lists * sizeof(mvb_result), false) ||
-        (prev && !HostCtx::grow(c.d_prev, c.prev_cap, n_lists * 4, false)))
+    if (!c.grow(c.d_in, c.in_cap, in_len, false) ||
+        !c.grow(c.d_out, c.out_cap, static_cast<size_t>(n_out) * 4, false) ||
+        !c.grow(c.d_ws, c.ws_cap, mvb_workspace_bytes(0), true) ||
+        !c.grow(c.d_bo, c.bo_cap, (n_lists + 1) * 8, false) ||
+        !c.grow(c.d_io, c.io_cap, (n_lists + 1) * 8, false) ||
+        !c.grow(c.d_lres, c.lres_cap, n_lists * sizeof(mvb_result), false) ||
+        (prev && !c.grow(c.d_prev, c.prev_cap, n_lists * 4, false)))
         return MVB_ERR_CUDA;
     // sub-batches [lb[b], lb[b + 1])
     size_t lb[65];
@@ -1117,30 +959,6 @@ int mvb_encode_deltas(const uint32_t* sorted_values, size_t n, uint8_t* out, siz
     return 0;
 }
 
-// Internal profiling entry (not part of include/mvb_cuda.h): a decode that
-// also records a per-tile timeline (8 x u64 per tile, %globaltimer ns).
-int mvbx_decode_traced(const uint8_t* in, size_t in_len, size_t count, int delta, uint32_t prev, uint32_t* out,
-                       int mode, mvb_result* res_dev, void* ws, size_t ws_bytes, mvb_stream_t stream,
-                       unsigned long long* trace) {
-    return decode_device(in, in_len, count, delta != 0, prev, out, mode, res_dev, ws, ws_bytes, stream, trace);
-}
-
-#if MVB_TRACE_B
-// Internal profiling entry (trace builds only): kernel B's per-warp timeline buffer.
-int mvbx_set_trace_b(unsigned long long* buf) {
-    return cudaMemcpyToSymbol(mvbk::mvb_trace_b, &buf, sizeof(buf)) == cudaSuccess ? 0 : MVB_ERR_CUDA;
-}
-#endif
-
-#if MVB_PATH_STATS
-// Internal profiling entry (path-stats builds only): slices per path since the last call.
-int mvbx_path_counts(unsigned long long* out4) {
-    if (cudaMemcpyFromSymbol(out4, mvbk::mvb_path_counts, 4 * sizeof(unsigned long long)) != cudaSuccess) return -1;
-    const unsigned long long z[4] = {0, 0, 0, 0};
-    return cudaMemcpyToSymbol(mvbk::mvb_path_counts, z, sizeof z) == cudaSuccess ? 0 : -1;
-}
-#endif
-
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
 
@@ -1173,9 +991,9 @@ void mvbx_set_host_pipeline(size_t min_bytes, size_t chunk_bytes, int grow) {
 // Kernels one decode call launches in steady state (bench accounting; the
 // workspace re-zeroing memset runs only when a workspace changes layout).
 int mvbx_kernels_per_decode(int mode) {
-    return (mode == MVB_STRICT && (g_kernel_choice == 5 || g_kernel_choice == 6)) ? 2 : 1;
+    return (mode == MVB_STRICT && g_kernel_choice == 6) ? 2 : 1;
 }
 
-const char* mvb_version(void) { return "mvb_cuda 0.2 (sm_100a, segmented lane-local VByte decoder)"; }
+const char* mvb_version(void) { return "mvb_cuda 0.3 (sm_100a, single-read fused VByte decoder)"; }
 
 }  // extern "C"

@@ -20,7 +20,7 @@ import io
 import os
 import struct
 from dataclasses import dataclass
-from typing import Iterable, List, Sequence, Union
+from typing import Optional, Iterable, List, Sequence, Union
 
 import numpy as np
 
@@ -58,8 +58,11 @@ def payload_is_canonical(payload: np.ndarray, count: int) -> bool:
     return True
 
 
-def write_list(sink, buf: EncodedBuffer, delta_coded: bool = True) -> int:
-    """list_file.cpp:44-55: header + payload; returns the bytes written."""
+def write_list(sink, buf: EncodedBuffer, delta_coded: Optional[bool] = None) -> int:
+    """list_file.cpp:44-55: header + payload; returns the bytes written.  The
+    flag is the buffer's own delta_coded (list_file.cpp:50) unless given."""
+    if delta_coded is None:
+        delta_coded = bool(buf.delta_coded)
     payload = np.ascontiguousarray(buf.bytes, np.uint8)
     if payload.size > 0xFFFFFFFF:
         raise ListFileError("write_list: payload exceeds 32-bit length")
@@ -68,7 +71,7 @@ def write_list(sink, buf: EncodedBuffer, delta_coded: bool = True) -> int:
     return HEADER_BYTES + payload.size
 
 
-def write_list_file(path, buf: EncodedBuffer, delta_coded: bool = True) -> int:
+def write_list_file(path, buf: EncodedBuffer, delta_coded: Optional[bool] = None) -> int:
     with open(path, "wb") as f:
         return write_list(f, buf, delta_coded)
 
@@ -94,7 +97,7 @@ def read_list(source, validate_payload: bool = True) -> ListRecord:
     b = np.frombuffer(payload, np.uint8)
     if validate_payload and not payload_is_canonical(b, count):
         raise ListFileError(f"read_list: payload is not {count} canonical integers")
-    return ListRecord(EncodedBuffer(b, count), (flags & 1) != 0)
+    return ListRecord(EncodedBuffer(b, count, (flags & 1) != 0), (flags & 1) != 0)
 
 
 def read_list_file(path, validate_payload: bool = True) -> ListRecord:

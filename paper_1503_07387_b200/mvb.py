@@ -169,6 +169,33 @@ def _mode_of(options) -> int:
     return int(DecodeMode(options))
 
 
+def _check_in_tensor(inp, n: int) -> None:
+    """A device input must be a contiguous uint8 CUDA tensor with >= n bytes."""
+    torch = inp.__class__.__module__.startswith("torch") and __import__("torch")
+    if not torch or not inp.is_cuda or inp.dtype != torch.uint8 or not inp.is_contiguous():
+        raise MvbError("device input must be a contiguous uint8 CUDA tensor")
+    if inp.numel() < n:
+        raise MvbError("device input holds fewer than in_len bytes")
+
+
+def _check_out_tensor(out, count: int, device) -> None:
+    """A device output must be a contiguous int32/uint32 CUDA tensor on the
+    input's device with >= count elements: the kernels write count*4
+    contiguous bytes from out.data_ptr()."""
+    if count == 0:
+        return
+    import torch
+
+    if out is None or not isinstance(out, torch.Tensor) or not out.is_cuda:
+        raise MvbError("decode on CUDA tensors needs a CUDA output tensor")
+    if out.dtype not in (torch.int32, torch.uint32) or not out.is_contiguous():
+        raise MvbError("device output must be a contiguous int32/uint32 tensor")
+    if out.device != device:
+        raise MvbError("device output must be on the input's device")
+    if out.numel() < count:
+        raise MvbError("device output holds fewer than count elements")
+
+
 class Decoder:
     """Device-side decoder state: a workspace and a result slot on one GPU.
 
@@ -198,6 +225,8 @@ class Decoder:
 
     def decode(self, inp, count: int, out, mode: int = 0, in_len: Optional[int] = None) -> None:
         n = inp.numel() if in_len is None else int(in_len)
+        _check_in_tensor(inp, n)
+        _check_out_tensor(out, int(count), inp.device)
         self._ensure(n)
         _check(_lib.lib().mvb_decode_device(
             inp.data_ptr() if n else None, n, int(count), out.data_ptr() if count else None, int(mode),
@@ -205,6 +234,8 @@ class Decoder:
 
     def decode_delta(self, inp, count: int, prev: int, out, mode: int = 0, in_len: Optional[int] = None) -> None:
         n = inp.numel() if in_len is None else int(in_len)
+        _check_in_tensor(inp, n)
+        _check_out_tensor(out, int(count), inp.device)
         self._ensure(n)
         _check(_lib.lib().mvb_decode_delta_device(
             inp.data_ptr() if n else None, n, int(count), int(prev) & 0xFFFFFFFF,
@@ -220,6 +251,23 @@ class Decoder:
         ``results`` (optional, int64 CUDA tensor of n*3) receives each list's
         DecodeResult as (status, values_written, bytes_consumed)."""
         n = int(byte_offsets.numel()) - 1
+        import torch
+
+        _check_in_tensor(inp, inp.numel())
+        for name, t in (("byte_offsets", byte_offsets), ("int_offsets", int_offsets)):
+            if not (t.is_cuda and t.dtype == torch.int64 and t.is_contiguous() and t.numel() == n + 1):
+                raise MvbError(f"{name} must be a contiguous int64 CUDA tensor of n_lists + 1 entries")
+        if prev is not None and not (prev.is_cuda and prev.dtype in (torch.int32, torch.uint32) and
+                                     prev.is_contiguous() and prev.numel() >= n):
+            raise MvbError("prev must be a contiguous int32/uint32 CUDA tensor of >= n_lists entries")
+        if results is not None and not (results.is_cuda and results.dtype == torch.int64 and
+                                        results.is_contiguous() and results.numel() >= 3 * n):
+            raise MvbError("results must be a contiguous int64 CUDA tensor of >= 3 * n_lists entries")
+        if n > 0:
+            io_h = int_offsets.cpu()
+            if bool((io_h[1:] < io_h[:-1]).any()) or bool((byte_offsets[1:] < byte_offsets[:-1]).any()):
+                raise MvbError("byte_offsets and int_offsets must be non-decreasing")
+            _check_out_tensor(out, int(io_h[-1]), inp.device)
         L = _lib.lib()
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         if delta:
@@ -255,8 +303,8 @@ def _decode(inp, count, prev, out, options, delta: bool):
     mode = _mode_of(options)
     count = int(count)
     if _is_cuda_tensor(inp):
-        if count and (out is None or not _is_cuda_tensor(out) or out.numel() < count):
-            raise MvbError("decode on CUDA tensors needs a CUDA output tensor with >= count elements")
+        _check_in_tensor(inp, inp.numel())
+        _check_out_tensor(out, count, inp.device)
         d = _decoder_for(inp)
         if delta:
             d.decode_delta(inp, count, prev, out, mode)
@@ -296,9 +344,13 @@ def decode_lists(inp, byte_offsets, int_offsets, out, prev=None, delta: bool = T
         raise MvbError("byte_offsets and int_offsets need the same length (n_lists + 1)")
     if not (isinstance(out, np.ndarray) and out.dtype in (np.uint32, np.int32) and out.flags.c_contiguous):
         raise MvbError("output must be a C-contiguous numpy uint32 array")
+    if n > 0 and (np.any(bo[1:] < bo[:-1]) or np.any(io[1:] < io[:-1])):
+        raise MvbError("byte_offsets and int_offsets must be non-decreasing")
     if n > 0 and out.size < int(io[-1]):
         raise MvbError("output array smaller than int_offsets[-1]")
     pv = None if prev is None else np.ascontiguousarray(prev, np.uint32)
+    if pv is not None and pv.size < n:
+        raise MvbError("prev needs one value per list")
     res = np.zeros((max(n, 1), 3), np.uint64) if results else None
     L = _lib.lib()
     if delta:

@@ -77,6 +77,25 @@ def resync(buf: np.ndarray, buf_lo: int, cut: int, total_len: int, halo: int = H
     return cut + int(hits[0]), True
 
 
+def list_ranges(byte_off: Sequence[int], world: int) -> List[int]:
+    """Cut a batch of independent lists (BASELINE.json config 3) into `world`
+    contiguous list ranges balanced by compressed bytes (the
+    lists are independent units, so no exchange is needed).  Returns
+    world + 1 list indices; rank r decodes lists [cuts[r], cuts[r+1]), whose
+    output offsets are int_off[cuts[r]] ... in the whole batch's output."""
+    bo = np.asarray(byte_off, dtype=np.int64)
+    n = bo.size - 1
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    total = int(bo[-1] - bo[0])
+    targets = [int(bo[0]) + (total * r) // world for r in range(world + 1)]
+    cuts = [int(np.searchsorted(bo[:n + 1], t, side="left")) for t in targets]
+    cuts[0], cuts[-1] = 0, n
+    for r in range(1, world + 1):  # monotone even for empty ranges
+        cuts[r] = max(cuts[r], cuts[r - 1])
+    return cuts
+
+
 @dataclass
 class ShardPlan:
     rank: int

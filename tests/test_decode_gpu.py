@@ -283,7 +283,7 @@ def test_config4_full_size_device(golden, oracle, cuda):
     assert oracle.fnv_u32(got) == s["out_fnv"]
 
 
-@pytest.mark.parametrize("choice", [1, 2, 3, 4, 5, 6, 0])
+@pytest.mark.parametrize("choice", [1, 6, 0])
 def test_every_strict_kernel_variant(choice, golden, oracle):
     """All strict-mode kernels (per-tile, warp-tile, CTA-pipelined, warp-sliced) agree with
     the oracle on KATs, errors across tile boundaries and a full config."""
@@ -338,7 +338,7 @@ def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
         v = W.mixed_values(n, seed)
         streams.append((v, oracle.encode_sequence(v)))
     try:
-        for choice in (0, 4, 1, 3, 2, 5, 6, 0):
+        for choice in (0, 1, 6, 0):
             _lib.set_kernel_choice(choice)
             for rep in range(2):
                 for (v, enc), mode in zip(streams * 2, [STRICT] * 5 + [PERMISSIVE] * 5):
@@ -353,7 +353,7 @@ def test_workspace_reuse_across_sizes_modes_and_kernels(cuda, oracle):
         _lib.set_kernel_choice(0)
 
 
-@pytest.mark.parametrize("choice", [0, 5])
+@pytest.mark.parametrize("choice", [0, 6])
 @pytest.mark.parametrize("delta", [True, False])
 def test_batched_lists_equal_per_list_oracle(cuda, oracle, delta, choice):
     """mvb_decode[_delta]_lists_device against one oracle decode per list,

@@ -41,6 +41,24 @@ def test_writer_and_reader_match_reference(tmp_path):
         assert np.array_equal(rec.buf.bytes, buf.bytes) and rec.buf.count == buf.count and rec.delta_coded
 
 
+@ref_needed
+def test_default_flag_is_the_buffers_own(tmp_path):
+    """write_list without an explicit flag writes buf.delta_coded
+    (list_file.cpp:50), and read_list hands it back on the EncodedBuffer."""
+    ref = RefLib()
+    ids = np.array([3, 9, 200, 70000, 70001], np.uint32)
+    for buf, want in ((mvb.encode_sequence(ids), False), (mvb.encode_deltas(ids), True)):
+        path = tmp_path / f"d{int(want)}.mvb"
+        LF.write_list_file(path, buf)
+        got = ref.read_list_file(path)
+        assert got is not None and got[2] == want
+        rec = LF.read_list_file(path)
+        assert rec.delta_coded == want and rec.buf.delta_coded == want
+        again = tmp_path / f"a{int(want)}.mvb"
+        LF.write_list_file(again, rec.buf)
+        assert again.read_bytes() == path.read_bytes()
+
+
 def _corruptions():
     good = mvb.encode_sequence(np.array([1, 300, 70000, 1 << 22, 0xFFFFFFFF], np.uint32))
     b = np.asarray(good.bytes, np.uint8)
