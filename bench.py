@@ -321,6 +321,12 @@ def run_reference(args):
         sample = (f"each step: ~0.5 s of list decodes (mvb::decode_delta_stream per list, runner.cpp decode_list), "
                   f"lists split over {threads} threads")
     else:
+        # One stream: the reference decodes a stream on one thread and has no way
+        # to split it (runner.cpp:174-196 times one thread per
+        # stream), so the arm times one thread on the stream's first
+        # SAMPLE_INTS integers.  The aggregate of `threads` threads each decoding
+        # its own replica -- a different workload, many streams -- is reported
+        # beside it (replicas_all_threads).
         k = vals.size
         outs = [np.empty(k + 16, np.uint32) for _ in range(threads)]
         dec = (lambda o: ref.decode_delta_stream(enc, k, h["prev"], out=o)) if h["delta"] else \
@@ -329,13 +335,13 @@ def run_reference(args):
         exp = (np.cumsum(vals, dtype=np.uint64) + np.uint64(h["prev"])).astype(np.uint32) if h["delta"] else vals
         assert r[0] == 0 and r[1] == k and np.array_equal(o, exp), "reference decode disagrees with ground truth"
 
-        def step():
+        def step(nthreads):
             def work(i):
                 r, _ = dec(outs[i])
                 assert r[0] == 0
 
             t0 = time.perf_counter()
-            ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+            ths = [threading.Thread(target=work, args=(i,)) for i in range(nthreads)]
             for t in ths:
                 t.start()
             for t in ths:
@@ -343,12 +349,19 @@ def run_reference(args):
             return time.perf_counter() - t0
 
         for _ in range(args.warmup):
-            step()
-        t_steps = [step() for _ in range(args.steps)]
-        value = k * threads * args.steps / sum(t_steps) / 1e9
-        sample = (f"each step: {threads} threads x 1 decode of the first {k} integers of the {h['name']} stream "
+            step(1)
+        t_steps = [step(1) for _ in range(args.steps)]
+        value = k * args.steps / sum(t_steps) / 1e9
+        for _ in range(max(1, args.warmup)):
+            step(threads)
+        t_rep = [step(threads) for _ in range(args.steps)]
+        replicas = {"value": k * threads * args.steps / sum(t_rep) / 1e9, "unit": UNIT, "threads": threads,
+                    "sample": f"each step: {threads} threads x 1 decode of their own replica of the sample "
+                              "(many independent streams: not this config's one stream)"}
+        sample = (f"each step: 1 thread x 1 decode of the first {k} integers of the {h['name']} stream "
                   f"(reference encoder's bytes) with mvb::decode{'_delta' if h['delta'] else ''}_stream "
-                  "(SSE masked path)")
+                  "(SSE masked path); one stream cannot be split across threads")
+        threads = 1
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(t_steps) / args.steps,
@@ -358,6 +371,8 @@ def run_reference(args):
                          "cpu_model": model},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if io is None:
+        line["replicas_all_threads"] = replicas
     print(json.dumps(line), flush=True)
 
 

@@ -312,11 +312,37 @@ __device__ __forceinline__ void lane_slots_d3(uint32_t wp3, const uint32_t (&w)[
     }
 }
 
+// One predicated staging store keyed on word w: if byte `bit` of w is a
+// terminator (its high bit, given as the mask, clear), stage[sp] = v, sp += 4.
+template <bool kSwz>
+__device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t hibit, uint32_t v) {
+    if (kSwz)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 t, a;\n\t"
+            "and.b32 t, %1, %2;\n\tsetp.eq.b32 p, t, 0;\n\t"
+            "shr.b32 a, %0, 3;\n\tand.b32 a, a, 0x70;\n\txor.b32 a, a, %0;\n\t"
+            "@p st.shared.u32 [a], %3;\n\t@p add.u32 %0, %0, 4;\n\t}"
+            : "+r"(sp)
+            : "r"(w), "r"(hibit), "r"(v)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %1, %2;\n\tsetp.eq.b32 p, t, 0;\n\t"
+            "@p st.shared.u32 [%0], %3;\n\t@p add.u32 %0, %0, 4;\n\t}"
+            : "+r"(sp)
+            : "r"(w), "r"(hibit), "r"(v)
+            : "memory");
+}
+
 // A delta unit staged in shared memory whose integers all have at most 3
 // bytes, with integer limit-1 outside it (both known from its totals pass):
 // every slice takes the dp2a path with no range masks, votes or limit checks.
 // carry: every byte before the unit (the prefix tree's sums count bytes, so
-// no straddle correction); values go to out[base ...].
+// no straddle correction); values go to out[base ...].  Per lane and word:
+// the continuation bits, the weights, the terminator count (one dp4a) and the
+// word's total; then the count and sum scans; then one dp2a and one
+// predicated store per byte.
 template <bool kSwz>
 __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, int n_slices, unsigned long long base, uint32_t carry,
                                                unsigned long long limit, uint32_t* out, uint32_t* stage, int lane) {
@@ -335,8 +361,22 @@ __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, int n_slices, unsi
         const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31);
         if (lane == 0) wp3 = pw;
         pw = l3;
-        const uint32_t T32 = hibits16(~w[0], ~w[1], ~w[2], ~w[3]) | (hibits16(~w[4], ~w[5], ~w[6], ~w[7]) << 16);
-        const uint32_t n_own = __popc(T32);
+        uint32_t W01[8], W23[8], w7[8], tk[8];
+        uint32_t cp = wp3 & 0x80808080u, cc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t ck = w[k] & 0x80808080u;
+            cc = __dp4a(ck, 0x01010101u, cc);  // 128 per continuation byte
+            // byte j: 1 if byte j-1 continues, 0x81 if bytes j-1 and j-2 do
+            const uint32_t x = __funnelshift_l(cp, ck, 1) | (__funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16));
+            // 16-bit weights 1 + 127 x: 1, 128, 16384
+            W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
+            W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
+            w7[k] = w[k] ^ ck;
+            tk[k] = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], 0u));
+            cp = ck;
+        }
+        const uint32_t n_own = 32u - (cc >> 7);
         uint32_t incl = n_own;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -344,7 +384,22 @@ __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, int n_slices, unsi
             if (lane >= o) incl += y;
         }
         const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        lane_slots_d3<kSwz>(wp3, w, T32, st_base + 4u * (a + incl - n_own), carry);
+        uint32_t tot = tk[0];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) tot += tk[k];
+        uint32_t acc = lane_scan_offset<true>(tot, carry);
+        uint32_t sp = st_base + 4u * (a + incl - n_own);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
+            const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
+            const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
+            acc += tk[k];
+            slot_store_w<kSwz>(sp, w[k], 0x80u, o0);
+            slot_store_w<kSwz>(sp, w[k], 0x8000u, o1);
+            slot_store_w<kSwz>(sp, w[k], 0x800000u, o2);
+            slot_store_w<kSwz>(sp, w[k], 0x80000000u, acc);
+        }
         __syncwarp();
         stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
         run += n_w;
