@@ -53,7 +53,9 @@ namespace mvbk {
 constexpr int kFBlocks = MVB_F_BLOCKS;
 constexpr int kUnit = MVB_F_UNIT;
 constexpr int kUnitBuf = (16 + kUnit + 127) / 128 * 128;      // 16 halo bytes + the unit
-constexpr int kFWarpBytes = 2 * kUnitBuf + 4 * kLaneStage;    // two unit buffers + the slice staging
+constexpr int kFStage = 1152;                                 // staging words: a slice of <= 1120 integers + alignment
+static_assert(kFStage >= kLaneStage, "staging serves decode_unit_ll too");
+constexpr int kFWarpBytes = 2 * kUnitBuf + 4 * kFStage;       // two unit buffers + the slice staging
 constexpr int kFSmem = kSegWarps * kFWarpBytes + 16 * kSegWarps;  // + two mbarriers per warp
 constexpr int kFLevels = 6;                                   // tree levels: up to 32^6 units
 static_assert(kUnit % 1024 == 0 && kFWarpBytes % 128 == 0, "unit geometry");
@@ -335,76 +337,97 @@ __device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t 
             : "memory");
 }
 
+// ---- fast delta units: odd lane strides ----
+//
+// Bank conflicts of the staging stores decide these slices' speed: with
+// 32-byte lanes, dense data puts the k-th output of every lane 32 words
+// apart, i.e. in one bank (the XOR swizzle of decode_range_ll spreads them
+// over 8 banks -- still 4-way).  Here a lane takes 4 * kNW - 1 bytes, an odd
+// stride, so the k-th outputs of dense lanes fall in distinct banks; the
+// staging is plain (no per-store swizzle).  A 4 KiB unit is three 992-byte
+// slices of 31-byte lanes and one 1120-byte slice of 35-byte lanes.  Each
+// lane reads its bytes and the 4 before them from the unit buffer with
+// word loads and funnel shifts; its last word's top byte (the next lane's
+// first) is masked out as a digit-0 continuation byte.
+
+// One d3 slice at unit offset `off` (bytes) with lanes of 4 * kNW - 1 bytes.
+template <int kNW>
+__device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, unsigned long long& run,
+                                             uint32_t out_w, unsigned long long limit, uint32_t* out, uint32_t& carry,
+                                             int lane) {
+    constexpr int kStride = 4 * kNW - 1;
+    const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
+    // the lane's bytes [b0, b0 + kStride) and the 4 before them
+    const uint32_t h0 = ubuf + off + static_cast<uint32_t>(kStride * lane) - 4u;
+    const uint32_t sh = 8u * (h0 & 3u);
+    const uint32_t wa = h0 & ~3u;
+    uint32_t r[kNW + 2];
+#pragma unroll
+    for (int k = 0; k < kNW + 2; ++k) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r[k]) : "r"(wa + 4u * k) : "memory");
+    uint32_t w[kNW + 1];
+#pragma unroll
+    for (int k = 0; k < kNW + 1; ++k) w[k] = __funnelshift_r(r[k], r[k + 1], sh);
+    // w[0]: the 4 bytes before; w[1 .. kNW]: the lane's bytes, the last one the next lane's
+    w[kNW] |= 0x80000000u;
+    uint32_t W01[kNW], W23[kNW], w7[kNW], tk[kNW];
+    uint32_t cp = w[0] & 0x80808080u, cc = 0;
+#pragma unroll
+    for (int k = 0; k < kNW; ++k) {
+        const uint32_t ck = w[k + 1] & 0x80808080u;
+        cc = __dp4a(ck, 0x01010101u, cc);  // 128 per continuation byte
+        // byte j: 1 if byte j-1 continues, 0x81 if bytes j-1 and j-2 do
+        const uint32_t x = __funnelshift_l(cp, ck, 1) | (__funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16));
+        W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
+        W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
+        w7[k] = w[k + 1] ^ ck;
+        if (k == kNW - 1) w7[k] &= 0x00FFFFFFu;  // (the next lane's byte weighs nothing)
+        tk[k] = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], 0u));
+        cp = ck;
+    }
+    const uint32_t n_own = 4u * kNW - (cc >> 7);
+    uint32_t incl = n_own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    uint32_t tot = tk[0];
+#pragma unroll
+    for (int k = 1; k < kNW; ++k) tot += tk[k];
+    uint32_t acc = lane_scan_offset<true>(tot, carry);
+    uint32_t sp = st_base + 4u * (a + incl - n_own);
+#pragma unroll
+    for (int k = 0; k < kNW; ++k) {
+        const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
+        const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
+        const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
+        acc += tk[k];
+        slot_store_w<false>(sp, w[k + 1], 0x80u, o0);
+        slot_store_w<false>(sp, w[k + 1], 0x8000u, o1);
+        slot_store_w<false>(sp, w[k + 1], 0x800000u, o2);
+        slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc);
+    }
+    __syncwarp();
+    stage_out<false>(st_base, a, n_w, run, limit, out, lane);
+    run += n_w;
+    __syncwarp();  // the staging buffer is rewritten by the next slice
+}
+
 // A delta unit staged in shared memory whose integers all have at most 3
 // bytes, with integer limit-1 outside it (both known from its totals pass):
 // every slice takes the dp2a path with no range masks, votes or limit checks.
 // carry: every byte before the unit (the prefix tree's sums count bytes, so
-// no straddle correction); values go to out[base ...].  Per lane and word:
-// the continuation bits, the weights, the terminator count (one dp4a) and the
-// word's total; then the count and sum scans; then one dp2a and one
-// predicated store per byte.
-template <bool kSwz>
-__device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, int n_slices, unsigned long long base, uint32_t carry,
+// no straddle correction); values go to out[base ...].
+__device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, unsigned long long base, uint32_t carry,
                                                unsigned long long limit, uint32_t* out, uint32_t* stage, int lane) {
+    static_assert(kUnit == 3 * 992 + 1120, "the d3 slicing covers a 4 KiB unit");
     const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
     const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     unsigned long long run = base;
-    uint32_t pw = 0;  // lane 0: the 4 bytes before the slice
-    if (lane == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(ubuf - 4u) : "memory");
 #pragma unroll 1
-    for (int i = 0; i < n_slices; ++i) {
-        const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
-        const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * i + 32 * lane);
-        const uint4 x0 = lds128(sa), x1 = lds128(sa + 16u);
-        const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-        uint32_t wp3 = __shfl_up_sync(0xFFFFFFFFu, w[7], 1);
-        const uint32_t l3 = __shfl_sync(0xFFFFFFFFu, w[7], 31);
-        if (lane == 0) wp3 = pw;
-        pw = l3;
-        uint32_t W01[8], W23[8], w7[8], tk[8];
-        uint32_t cp = wp3 & 0x80808080u, cc = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t ck = w[k] & 0x80808080u;
-            cc = __dp4a(ck, 0x01010101u, cc);  // 128 per continuation byte
-            // byte j: 1 if byte j-1 continues, 0x81 if bytes j-1 and j-2 do
-            const uint32_t x = __funnelshift_l(cp, ck, 1) | (__funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16));
-            // 16-bit weights 1 + 127 x: 1, 128, 16384
-            W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
-            W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
-            w7[k] = w[k] ^ ck;
-            tk[k] = dp2a_lo(W01[k], w7[k], dp2a_hi(W23[k], w7[k], 0u));
-            cp = ck;
-        }
-        const uint32_t n_own = 32u - (cc >> 7);
-        uint32_t incl = n_own;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t n_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        uint32_t tot = tk[0];
-#pragma unroll
-        for (int k = 1; k < 8; ++k) tot += tk[k];
-        uint32_t acc = lane_scan_offset<true>(tot, carry);
-        uint32_t sp = st_base + 4u * (a + incl - n_own);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
-            const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
-            const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
-            acc += tk[k];
-            slot_store_w<kSwz>(sp, w[k], 0x80u, o0);
-            slot_store_w<kSwz>(sp, w[k], 0x8000u, o1);
-            slot_store_w<kSwz>(sp, w[k], 0x800000u, o2);
-            slot_store_w<kSwz>(sp, w[k], 0x80000000u, acc);
-        }
-        __syncwarp();
-        stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
-        run += n_w;
-        __syncwarp();  // the staging buffer is rewritten by the next slice
-    }
+    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, run, out_w, limit, out, carry, lane);
+    slice_d3_odd<9>(ubuf, 2976u, st_base, run, out_w, limit, out, carry, lane);
 }
 
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
@@ -867,10 +890,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                     // every integer has at most 3 bytes, integer count-1 ends after the
                     // unit: the dp2a path throughout (carry: every byte before the unit)
                     const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
-                    if (swz)
-                        decode_unit_d3<true>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
-                    else
-                        decode_unit_d3<false>(ubuf, kUnit / kLLSlice, base, carry, S.count, S.out, stage, lane);
+                    decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane);
                 } else {
                     uint32_t straddle = 0;
                     if (kDelta) {
