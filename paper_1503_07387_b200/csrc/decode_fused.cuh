@@ -69,6 +69,7 @@ struct alignas(16) FEntry {
 struct FusedParams {
     SegParams S;                 // in, mis, len, count, out, prev, prev_dev, seg_bytes (= kUnit), n_seg, hdr, res_dev
     int swz;                     // staging swizzle: 0 never, 1 always, 2 dense units (debug switch)
+    int narrow;                  // every count fits 32 bits (stream < 4 GiB): warp sums by redux
     int levels;                  // tree levels in use (32^levels >= n_seg)
     long long n_at[kFLevels];    // entries per level (n_at[0] = n_seg)
     FEntry* tree[kFLevels];      // level arrays
@@ -621,13 +622,14 @@ __device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long 
         unsigned long long c = 0;
         uint32_t s = 0;
         if (lane < kids) fentry_get(F.tree[l] + (par << 5) + lane, tag, c, s);
+        sum = __reduce_add_sync(0xFFFFFFFFu, s);
+        if (F.narrow) {
+            cnt = __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(c));
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-            s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            cnt = c;
         }
-        cnt = c;
-        sum = s;
         i = par;
         ++l;
     }
@@ -638,7 +640,8 @@ __device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long 
 // published in this launch.
 __device__ __forceinline__ void fused_prefix(const FusedParams& F, long long v, unsigned tag, int lane,
                                              unsigned long long& cnt, unsigned long long& sum) {
-    unsigned long long c = 0, s = 0;
+    unsigned long long c = 0;
+    uint32_t s = 0;
     for (int l = 0; l < F.levels; ++l) {
         const long long d = (v >> (5 * l)) & 31;
         if (lane < d) {
@@ -649,13 +652,14 @@ __device__ __forceinline__ void fused_prefix(const FusedParams& F, long long v, 
             s += es;
         }
     }
+    sum = __reduce_add_sync(0xFFFFFFFFu, s);
+    if (F.narrow) {
+        cnt = __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(c));
+    } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        cnt = c;
     }
-    cnt = c;
-    sum = s;
 }
 
 // fused_totals for a unit staged in shared memory (ubuf: its first byte; the
