@@ -70,6 +70,7 @@ struct FusedParams {
     SegParams S;                 // in, mis, len, count, out, prev, prev_dev, seg_bytes (= kUnit), n_seg, hdr, res_dev
     int swz;                     // staging swizzle: 0 never, 1 always, 2 dense units (debug switch)
     int narrow;                  // every count fits 32 bits (stream < 4 GiB): warp sums by redux
+    int early;                   // many units per warp: load a unit's prefix entries before the next unit's totals
     int levels;                  // tree levels in use (32^levels >= n_seg)
     long long n_at[kFLevels];    // entries per level (n_at[0] = n_seg)
     FEntry* tree[kFLevels];      // level arrays
@@ -707,6 +708,52 @@ __device__ __forceinline__ void unit_totals(uint32_t ubuf, int n_it, int lane, u
     sum_out = kDelta ? __reduce_add_sync(0xFFFFFFFFu, sA + (sB << 14) + sX) : 0u;
 }
 
+// fused_prefix in two halves: the entries' loads are issued early (their
+// latency overlaps other work), the tags checked -- and stale entries
+// waited for -- later.
+struct PrefixLoads {
+    unsigned long long c[kFLevels], s[kFLevels];
+};
+__device__ __forceinline__ void fused_prefix_issue(const FusedParams& F, long long v, int lane, PrefixLoads& P) {
+#pragma unroll
+    for (int l = 0; l < kFLevels; ++l) {
+        P.c[l] = 0;
+        P.s[l] = 0;
+        if (l < F.levels && lane < ((v >> (5 * l)) & 31)) {
+            const FEntry* e = F.tree[l] + (((v >> (5 * l)) >> 5) << 5) + lane;
+            asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(P.c[l]), "=l"(P.s[l]) : "l"(e) : "memory");
+        }
+    }
+}
+__device__ __forceinline__ void fused_prefix_finish(const FusedParams& F, long long v, unsigned tag, int lane,
+                                                    PrefixLoads& P, unsigned long long& cnt, unsigned long long& sum) {
+    unsigned long long c = 0;
+    uint32_t s = 0;
+#pragma unroll
+    for (int l = 0; l < kFLevels; ++l) {
+        if (l < F.levels && lane < ((v >> (5 * l)) & 31)) {
+            unsigned long long ec;
+            uint32_t es;
+            if ((P.c[l] & 0xFFFFFFull) == tag && (P.s[l] & 0xFFFFFFull) == tag) {
+                ec = P.c[l] >> 24;
+                es = static_cast<uint32_t>(P.s[l] >> 32);
+            } else {
+                fentry_get(F.tree[l] + (((v >> (5 * l)) >> 5) << 5) + lane, tag, ec, es);
+            }
+            c += ec;
+            s += es;
+        }
+    }
+    sum = __reduce_add_sync(0xFFFFFFFFu, s);
+    if (F.narrow) {
+        cnt = __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(c));
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        cnt = c;
+    }
+}
+
 // Completion (all threads of every CTA): the last CTA produces the DecodeResult.
 __device__ __forceinline__ void fused_complete(const FusedParams& F, unsigned tag) {
     const SegParams& S = F.S;
@@ -864,12 +911,18 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         const int b = bp ^ 1;
         unsigned c_u = 0;
         uint32_t f_u = 0;
+        const long long qu = u * kUnit;
+        const bool u_staged = u < S.n_seg && qu - 16 >= R.lo && qu + kUnit <= R.hi;  // (warp-uniform)
+        if (u_staged && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qu - 16, kUnit + 16, bar0 + 8u * b);
+        // unit up's prefix entries: loads only (they were published long ago;
+        // checked after unit u's publication, so a wait never delays it)
+        PrefixLoads P;
+        if (up >= 0 && F.early) fused_prefix_issue(F, up, lane, P);
         if (u < S.n_seg) {
-            const long long qs = u * kUnit;
-            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
+            const long long qs = qu;
+            const bool staged = u_staged;
             uint32_t su;
             if (staged) {
-                if (lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qs - 16, kUnit + 16, bar0 + 8u * b);
                 while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
                 }
                 phases ^= 1u << b;
@@ -883,7 +936,8 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         // publication of unit u, which later units wait for) ----
         if (up >= 0) {
             unsigned long long base, csum;
-            fused_prefix(F, up, tag, lane, base, csum);
+            if (!F.early) fused_prefix_issue(F, up, lane, P);
+            fused_prefix_finish(F, up, tag, lane, P, base, csum);
             if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
                 const long long qs = up * kUnit;
                 const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
