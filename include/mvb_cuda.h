@@ -94,15 +94,6 @@ int mvb_decode_delta_device(const uint8_t *in, size_t in_len, size_t count, uint
                             uint32_t *out, int mode, mvb_result *res_dev, void *ws,
                             size_t ws_bytes, mvb_stream_t stream);
 
-/* Sharded-decode pre-pass: number of integers that END in
- * in[0..in_len) (terminator bytes) and the sum of their values mod 2^32,
- * written to device memory.  A shard of a longer stream, cut at integer
- * boundaries, is decoded with prev = the caller's running sum of the earlier
- * shards' totals -- the per-shard split of decode_delta_scalar's
- * `prev += value` (vbyte.cpp:63-74).  Asynchronous on `stream`. */
-int mvb_scan_totals_device(const uint8_t *in, size_t in_len, unsigned long long *count_dev,
-                           uint32_t *sum_dev, mvb_stream_t stream);
-
 /* mvb_decode_delta_device with the starting value read from device memory
  * when the kernel runs (prev = *prev_dev), so a carry computed on the device
  * (mvb_shard_carry_device) feeds the decode without a host round trip. */
@@ -113,7 +104,7 @@ int mvb_decode_delta_device_dprev(const uint8_t *in, size_t in_len, size_t count
 
 /* Seam fix-up of the sharded decode: from n_ranks all-gathered records of
  * record_words u64 each (word 0 = integer count, low 32 bits of word 1 = gap
- * sum, as written by mvb_scan_totals_device), writes shard `rank`'s carry-in
+ * sum, as written by mvb_delta_totals_device), writes shard `rank`'s carry-in
  * prev + sum[0..rank) mod 2^32 and its output offset count[0..rank).  Either
  * output may be NULL.  Asynchronous on `stream`. */
 int mvb_shard_carry_device(const unsigned long long *records, int n_ranks, int rank,
@@ -155,6 +146,45 @@ int mvb_decode_lists(const uint8_t *in, size_t in_len, const unsigned long long 
 int mvb_decode_delta_lists(const uint8_t *in, size_t in_len, const unsigned long long *byte_off,
                            const unsigned long long *int_off, const uint32_t *prev, size_t n_lists,
                            uint32_t *out, int mode, mvb_result *results);
+
+/* ------------------------------------------------------ sharded delta decode */
+
+/* A delta stream split by byte range over several GPUs (SURVEY.md §8e,
+ * BASELINE.json config 4): each shard's decode needs the gap sum of the
+ * shards before it.  The reference decodes one stream on one thread
+ * (decode.hpp:51-52); these split its decode_delta_stream.
+ *
+ * mvb_delta_totals_device: one read of in (the single-read decoder's totals
+ * pass, last unit first): rec_dev[0] = integers in in, rec_dev[1] = the sum
+ * of their values mod 2^32 (the gap sum).  The workspace keeps the per-unit
+ * totals for the decode pass: mvb_decode_delta_totaled_device must follow on
+ * the same stream with the same in, in_len and workspace (strict mode; it
+ * reads in again, the units the totals pass read last from L2).
+ * mvb_decode_delta_totaled_device: decode_delta_stream(in, count, prev +
+ * (prev_dev ? *prev_dev : 0)) with the totals already known. */
+int mvb_delta_totals_device(const uint8_t *in, size_t in_len, unsigned long long *rec_dev, void *ws,
+                            size_t ws_bytes, mvb_stream_t stream);
+int mvb_decode_delta_totaled_device(const uint8_t *in, size_t in_len, size_t count, uint32_t prev,
+                                    const uint32_t *prev_dev, uint32_t *out, mvb_result *res_dev, void *ws,
+                                    size_t ws_bytes, mvb_stream_t stream);
+
+/* Cut in (host bytes) into n shards at integer boundaries: cuts[0] = 0,
+ * cuts[n] = in_len, cuts[g] = the first integer start at or after
+ * in_len * g / n (a continuation run with no end stays whole in shard g-1). */
+int mvb_shard_cuts(const uint8_t *in, size_t in_len, int n, unsigned long long *cuts);
+
+/* decode_delta_stream(in, count, prev, out) of one stream held as n shards
+ * on n GPUs of this process (devices[g] may repeat: several shards on one
+ * GPU).  shard_in[g] / shard_len[g]: shard g's bytes, a device pointer on
+ * devices[g] -- consecutive pieces of the stream cut at integer boundaries
+ * (mvb_shard_cuts).  Shard g's values go to shard_out[g] (device, room for
+ * shard_len[g] values) and are out[offsets[g] ...] of the whole decode.  The
+ * shards but the last are totalled (one read each, concurrently), the 16-byte
+ * totals exchanged, then every shard decodes from its carry.  Returns the
+ * whole stream's DecodeResult (status; *res may be NULL), synchronously. */
+int mvb_decode_delta_sharded(int n, const int *devices, const uint8_t *const *shard_in, const size_t *shard_len,
+                             size_t count, uint32_t prev, uint32_t *const *shard_out, unsigned long long *offsets,
+                             mvb_result *res);
 
 /* ------------------------------------------------------------ host drop-ins */
 

@@ -19,7 +19,10 @@ EXPORTS = (
     "mvb_workspace_init",
     "mvb_decode_device",
     "mvb_decode_delta_device",
-    "mvb_scan_totals_device",
+    "mvb_delta_totals_device",
+    "mvb_decode_delta_totaled_device",
+    "mvb_shard_cuts",
+    "mvb_decode_delta_sharded",
     "mvb_decode_delta_device_dprev",
     "mvb_shard_carry_device",
     "mvb_decode_lists_device",
@@ -68,8 +71,6 @@ def _declare(lib):
     lib.mvb_decode_device.restype = i32
     lib.mvb_decode_delta_device.argtypes = [vp, sz, sz, u32, vp, i32, vp, vp, sz, vp]
     lib.mvb_decode_delta_device.restype = i32
-    lib.mvb_scan_totals_device.argtypes = [vp, sz, vp, vp, vp]
-    lib.mvb_scan_totals_device.restype = i32
     lib.mvb_decode_delta_device_dprev.argtypes = [vp, sz, sz, vp, vp, i32, vp, vp, sz, vp]
     lib.mvb_decode_delta_device_dprev.restype = i32
     lib.mvb_shard_carry_device.argtypes = [vp, i32, i32, i32, u32, vp, vp, vp]
@@ -102,6 +103,15 @@ def _declare(lib):
     lib.mvb_encode_sequence.restype = sz
     lib.mvb_encode_deltas.argtypes = [vp, sz, vp, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     lib.mvb_encode_deltas.restype = i32
+    if hasattr(lib, "mvb_delta_totals_device"):  # (older builds under MVB_CUDA_LIB lack the sharded entries)
+        lib.mvb_delta_totals_device.argtypes = [vp, sz, vp, vp, sz, vp]
+        lib.mvb_delta_totals_device.restype = i32
+        lib.mvb_decode_delta_totaled_device.argtypes = [vp, sz, sz, u32, vp, vp, vp, vp, sz, vp]
+        lib.mvb_decode_delta_totaled_device.restype = i32
+        lib.mvb_shard_cuts.argtypes = [vp, sz, i32, vp]
+        lib.mvb_shard_cuts.restype = i32
+        lib.mvb_decode_delta_sharded.argtypes = [i32, vp, vp, vp, sz, u32, vp, vp, ctypes.POINTER(MvbResult)]
+        lib.mvb_decode_delta_sharded.restype = i32
     lib.mvb_version.argtypes = []
     lib.mvb_version.restype = ctypes.c_char_p
     return lib

@@ -71,6 +71,8 @@ struct FusedParams {
     int swz;                     // staging swizzle: 0 never, 1 always, 2 dense units (debug switch)
     int narrow;                  // every count fits 32 bits (stream < 4 GiB): warp sums by redux
     int early;                   // many units per warp: load a unit's prefix entries before the next unit's totals
+    int mode;                    // 0 totals and decode, 1 totals only (-> rec), 2 decode only (totals of a mode-1 launch)
+    unsigned long long* rec;     // mode 1: the stream's [integer count, value sum]
     int levels;                  // tree levels in use (32^levels >= n_seg)
     long long n_at[kFLevels];    // entries per level (n_at[0] = n_seg)
     FEntry* tree[kFLevels];      // level arrays
@@ -588,8 +590,11 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
     ro.n = run - base;
 }
 
-__device__ __forceinline__ void fentry_put(FEntry* e, unsigned long long cnt, uint32_t sum, unsigned tag) {
-    const ulonglong2 v = make_ulonglong2((cnt << 24) | tag, (static_cast<unsigned long long>(sum) << 32) | tag);
+__device__ __forceinline__ void fentry_put(FEntry* e, unsigned long long cnt, uint32_t sum, unsigned tag,
+                                           uint32_t flags = 0u) {
+    // (bits 24..31 of the sum word: a unit's totals-pass flags, level 0 only)
+    const ulonglong2 v = make_ulonglong2((cnt << 24) | tag,
+                                         (static_cast<unsigned long long>(sum) << 32) | ((flags & 0xFFu) << 24) | tag);
     asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(e), "l"(v.x), "l"(v.y) : "memory");
 }
 // Wait for entry e of this launch (tag) and return its count and sum.
@@ -607,9 +612,9 @@ __device__ __forceinline__ void fentry_get(const FEntry* e, unsigned tag, unsign
 // Publish entry i of level l (one lane) and aggregate upwards: the last
 // child to arrive at a parent sums the parent's children (the whole warp).
 __device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long long i, unsigned long long cnt,
-                                              uint32_t sum, unsigned tag, int lane) {
+                                              uint32_t sum, unsigned tag, int lane, uint32_t flags = 0u) {
     for (;;) {
-        if (lane == 0) fentry_put(F.tree[l] + i, cnt, sum, tag);
+        if (lane == 0) fentry_put(F.tree[l] + i, cnt, sum, tag, l == 0 ? flags : 0u);
         if (l + 1 >= F.levels) return;
         const long long par = i >> 5;
         const unsigned kids = static_cast<unsigned>((F.n_at[l] - (par << 5)) < 32 ? F.n_at[l] - (par << 5) : 32);
@@ -771,11 +776,26 @@ __device__ __forceinline__ void fused_complete(const FusedParams& F, unsigned ta
     if (threadIdx.x < 32) {
         unsigned long long c, u;
         fused_prefix(F, S.n_seg, tag, threadIdx.x, c, u);
-        if (threadIdx.x == 0) s_total = c;
+        if (threadIdx.x == 0) {
+            s_total = c;
+            if (F.mode == 1) {  // a totals pass: the record, no DecodeResult
+                F.rec[0] = c;
+                F.rec[1] = u & 0xFFFFFFFFull;
+            }
+        }
     }
     __syncthreads();
     const unsigned long long total = s_total;
     WsHeader* h = S.hdr;
+    if (F.mode == 1) {
+        if (threadIdx.x == 0) {
+            h->done = 0;
+            h->ticket = 0;
+            h->epoch = h->epoch + 1;
+        }
+        __threadfence();
+        return;
+    }
     const unsigned long long err_inv = *reinterpret_cast<volatile unsigned long long*>(&h->err_idx_inv);
     const bool truncated = !(err_inv != 0ull && ~err_inv < S.count) && total < S.count;  // (CTA-uniform)
     long long last_end_found = 0;
@@ -866,7 +886,9 @@ __device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uin
                  : "memory");
 }
 
-template <bool kDelta>
+// kMode: 0 totals and decode, 1 totals only, 2 decode only (F.mode == kMode;
+// separate instantiations keep the common one free of the others' code)
+template <bool kDelta, int kMode>
 __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(const __grid_constant__ FusedParams F) {
     extern __shared__ __align__(128) uint8_t smem[];
     const SegParams& S = F.S;
@@ -891,89 +913,162 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     // visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const unsigned tag =
-        static_cast<unsigned>(*reinterpret_cast<volatile unsigned long long*>(&S.hdr->epoch) + 1ull) & 0xFFFFFFu;
+    // this launch's tree tag; a decode-only launch reads the tree its totals
+    // launch (the previous one on this workspace) tagged
+    const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(&S.hdr->epoch);
+    const unsigned tag = static_cast<unsigned>(kMode == 2 ? epoch : epoch + 1ull) & 0xFFFFFFu;
     const uint32_t prev0 = kDelta ? (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
-    // Pipeline per warp: take unit u, load it, total it and publish -- then
-    // decode the unit taken one iteration earlier (its predecessors took their
-    // tickets before it and published right after, so its prefix is out).
-    // The publication must follow the ticket closely: a unit is waited for by
-    // every later one.  (Taking the ticket before the previous unit's decode,
-    // to overlap the load with it, made later units wait a whole decode.)
-    long long up = -1;  // the unit awaiting its decode (buffer bp)
-    int bp = 0;
-    unsigned c_up = 0;  // its totals pass: integer count, flags
-    uint32_t f_up = 0;
-    for (;;) {
+    // decode unit `up` (buffer bp), given its prefix and its totals pass's count / flags
+    auto decode_unit = [&](long long up, int bp, unsigned long long base, unsigned long long csum, unsigned c_up,
+                           uint32_t f_up) {
+        if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
+            const long long qs = up * kUnit;
+            const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
+            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
+            const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
+            const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
+            if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
+                // every integer has at most 3 bytes, integer count-1 ends after the
+                // unit: the dp2a path throughout (carry: every byte before the unit)
+                const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
+                decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane);
+            } else {
+                uint32_t straddle = 0;
+                if (kDelta) {
+                    uint32_t wb;
+                    if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
+                    else wb = r_word(R, qs - 4);
+                    straddle = tail_value(wb);
+                }
+                const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
+                RangeOut ro;
+                if (swz)
+                    decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                 ro);
+                else
+                    decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                  ro);
+            }
+        }
+    };
+    auto load_unit = [&](long long u, int b) -> bool {  // TMA of unit u into buffer b (if inside the stream)
+        const long long q = u * kUnit;
+        const bool st = u < S.n_seg && q - 16 >= R.lo && q + kUnit <= R.hi;  // (warp-uniform)
+        if (st && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + q - 16, kUnit + 16, bar0 + 8u * b);
+        return st;
+    };
+    auto wait_unit = [&](int b) {
+        while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
+        }
+        phases ^= 1u << b;
+    };
+    if constexpr (kMode == 1) {
+        // totals only, last unit first: the decode pass that follows starts
+        // with the units read last, still in L2
+        for (;;) {
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
+            t = __shfl_sync(0xFFFFFFFFu, t, 0);
+            if (static_cast<long long>(t) >= S.n_seg) break;
+            const long long u = S.n_seg - 1 - static_cast<long long>(t);
+            unsigned c_u;
+            uint32_t su, f_u;
+            if (load_unit(u, 0)) {
+                wait_unit(0);
+                unit_totals<kDelta>(buf0 + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+            } else {
+                fused_totals<kDelta>(S, u * kUnit, u * kUnit + kUnit, lane, c_u, su, 0u, &f_u);
+            }
+            fused_publish(F, 0, u, c_u, su, tag, lane, f_u);
+            __syncwarp();
+        }
+        fused_complete(F, tag);
+        return;
+    }
+    if constexpr (kMode == 2) {
+        // decode only: every prefix is out; the next unit's bytes load while
+        // this one is decoded
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
-        const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
-        const int b = bp ^ 1;
-        unsigned c_u = 0;
-        uint32_t f_u = 0;
-        const long long qu = u * kUnit;
-        const bool u_staged = u < S.n_seg && qu - 16 >= R.lo && qu + kUnit <= R.hi;  // (warp-uniform)
-        if (u_staged && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qu - 16, kUnit + 16, bar0 + 8u * b);
-        // unit up's prefix entries: loads only (they were published long ago;
-        // checked after unit u's publication, so a wait never delays it)
-        PrefixLoads P;
-        if (up >= 0 && F.early) fused_prefix_issue(F, up, lane, P);
-        if (u < S.n_seg) {
-            const long long qs = qu;
-            const bool staged = u_staged;
-            uint32_t su;
-            if (staged) {
-                while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
-                }
-                phases ^= 1u << b;
-                unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
-            } else {
-                fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
-            }
-            fused_publish(F, 0, u, c_u, su, tag, lane);
+        long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+        int b = 0;
+        bool st = load_unit(u, b);
+        while (u < S.n_seg) {
+            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
+            const long long un = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+            const bool stn = load_unit(un, b ^ 1);
+            PrefixLoads P;
+            fused_prefix_issue(F, u, lane, P);
+            unsigned long long base, csum, c_e;
+            uint32_t s_e;
+            fused_prefix_finish(F, u, tag, lane, P, base, csum);
+            const FEntry* e = F.tree[0] + u;
+            fentry_get(e, tag, c_e, s_e);
+            const uint32_t f_e = static_cast<uint32_t>((__ldcg(&e->s) >> 24) & 0xFFu);
+            if (st) wait_unit(b);
+            if (base < S.count) decode_unit(u, b, base, csum, static_cast<unsigned>(c_e), f_e);
+            __syncwarp();  // (buffer b is refilled next iteration)
+            u = un;
+            st = stn;
+            b ^= 1;
         }
-        // ---- decode unit up (only now: a wait here must never hold back the
-        // publication of unit u, which later units wait for) ----
-        if (up >= 0) {
-            unsigned long long base, csum;
-            if (!F.early) fused_prefix_issue(F, up, lane, P);
-            fused_prefix_finish(F, up, tag, lane, P, base, csum);
-            if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
-                const long long qs = up * kUnit;
-                const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
-                const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
-                const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
-                const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
-                if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
-                    // every integer has at most 3 bytes, integer count-1 ends after the
-                    // unit: the dp2a path throughout (carry: every byte before the unit)
-                    const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
-                    decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane);
-                } else {
-                    uint32_t straddle = 0;
-                    if (kDelta) {
-                        uint32_t wb;
-                        if (ubuf) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
-                        else wb = r_word(R, qs - 4);
-                        straddle = tail_value(wb);
+        fused_complete(F, tag);
+        return;
+    }
+    if constexpr (kMode == 0) {
+        // Pipeline per warp: take unit u, load it, total it and publish -- then
+        // decode the unit taken one iteration earlier (its predecessors took their
+        // tickets before it and published right after, so its prefix is out).
+        // The publication must follow the ticket closely: a unit is waited for by
+        // every later one.  (Taking the ticket before the previous unit's decode,
+        // to overlap the load with it, made later units wait a whole decode.)
+        long long up = -1;  // the unit awaiting its decode (buffer bp)
+        int bp = 0;
+        unsigned c_up = 0;  // its totals pass: integer count, flags
+        uint32_t f_up = 0;
+        for (;;) {
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
+            const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+            const int b = bp ^ 1;
+            unsigned c_u = 0;
+            uint32_t f_u = 0;
+            const long long qu = u * kUnit;
+            const bool u_staged = u < S.n_seg && qu - 16 >= R.lo && qu + kUnit <= R.hi;  // (warp-uniform)
+            if (u_staged && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qu - 16, kUnit + 16, bar0 + 8u * b);
+            // unit up's prefix entries: loads only (they were published long ago;
+            // checked after unit u's publication, so a wait never delays it)
+            PrefixLoads P;
+            if (up >= 0 && F.early) fused_prefix_issue(F, up, lane, P);
+            if (u < S.n_seg) {
+                const long long qs = qu;
+                const bool staged = u_staged;
+                uint32_t su;
+                if (staged) {
+                    while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
                     }
-                    const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
-                    RangeOut ro;
-                    if (swz)
-                        decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
-                                                     ro);
-                    else
-                        decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
-                                                      ro);
+                    phases ^= 1u << b;
+                    unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+                } else {
+                    fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
                 }
+                fused_publish(F, 0, u, c_u, su, tag, lane, f_u);
             }
-            __syncwarp();  // (buffer bp is refilled next iteration)
+            // ---- decode unit up (only now: a wait here must never hold back the
+            // publication of unit u, which later units wait for) ----
+            if (up >= 0) {
+                unsigned long long base, csum;
+                if (!F.early) fused_prefix_issue(F, up, lane, P);
+                fused_prefix_finish(F, up, tag, lane, P, base, csum);
+                decode_unit(up, bp, base, csum, c_up, f_up);
+                __syncwarp();  // (buffer bp is refilled next iteration)
+            }
+            if (u >= S.n_seg) break;
+            up = u;
+            bp = b;
+            c_up = c_u;
+            f_up = f_u;
         }
-        if (u >= S.n_seg) break;
-        up = u;
-        bp = b;
-        c_up = c_u;
-        f_up = f_u;
     }
     fused_complete(F, tag);
 }

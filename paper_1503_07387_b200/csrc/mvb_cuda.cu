@@ -13,6 +13,8 @@
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
+#include <deque>
 
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
@@ -301,10 +303,11 @@ FusedPlan fused_plan(long long qlen, long long W_max) {
     return f;
 }
 
-template <bool Delta>
-int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
+template <bool Delta, int Mode>
+int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, unsigned long long* rec) {
+    constexpr int mode = Mode;
     int sms = 0;
-    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta>), mvbk::kSegThreads,
+    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode>), mvbk::kSegThreads,
                                  mvbk::kFSmem, &sms);
     if (per_sm < 0) return MVB_ERR_CUDA;
     const long long W_max = static_cast<long long>(per_sm) * sms * mvbk::kSegWarps;
@@ -327,6 +330,8 @@ int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     F.narrow = (p.mis + p.len) < (1ll << 32) ? 1 : 0;
     // (a stream of few units per warp: the entries are rarely out that early)
     F.early = f.n_seg >= 16 * f.W ? 1 : 0;
+    F.mode = mode;
+    F.rec = rec;
     F.levels = f.levels;
     char* b = static_cast<char*>(ws) + kHeaderBytes;
     for (int l = 0; l < f.levels; ++l) {
@@ -349,8 +354,16 @@ int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta>, F) != cudaSuccess) return MVB_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode>, F) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+template <bool Delta>
+int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, int mode = 0,
+                 unsigned long long* rec = nullptr) {
+    if (mode == 1) return launch_fused_m<true, 1>(p, ws, ws_bytes, s, rec);
+    if (mode == 2) return launch_fused_m<true, 2>(p, ws, ws_bytes, s, rec);
+    return launch_fused_m<Delta, 0>(p, ws, ws_bytes, s, rec);
 }
 
 int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
@@ -410,6 +423,48 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
         e = mode == MVB_STRICT ? launch<false, mvbk::MODE_STRICT>(p, stream)
                                : launch<false, mvbk::MODE_PERMISSIVE>(p, stream);
     return e == cudaSuccess ? 0 : MVB_ERR_CUDA;
+}
+
+// Totals pass / decode pass of the single-read decoder (sharded delta decode:
+// a shard's gap sum is needed by the shards after it before they decode).
+int delta_totals_device(const uint8_t* in, size_t in_len, unsigned long long* rec_dev, void* ws, size_t ws_bytes,
+                        cudaStream_t stream) {
+    if ((in == nullptr && in_len > 0) || rec_dev == nullptr) return MVB_ERR_INVALID_ARG;
+    if (in_len == 0) return cudaMemsetAsync(rec_dev, 0, 16, stream) == cudaSuccess ? 0 : MVB_ERR_CUDA;
+    if (in_len >= (1ull << 40)) return MVB_ERR_INVALID_ARG;
+    if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
+    Params p = {};
+    p.in = in;
+    p.mis = static_cast<long long>(reinterpret_cast<uintptr_t>(in) & 15u);
+    p.len = static_cast<long long>(in_len);
+    p.count = in_len;
+    p.hdr = static_cast<WsHeader*>(ws);
+    return launch_fused<true>(p, ws, ws_bytes, stream, 1, rec_dev);
+}
+
+int delta_totaled_device(const uint8_t* in, size_t in_len, size_t count, uint32_t prev, const uint32_t* prev_dev,
+                         uint32_t* out, mvb_result* res_dev, void* ws, size_t ws_bytes, cudaStream_t stream) {
+    if ((in == nullptr && in_len > 0) || (out == nullptr && count > 0)) return MVB_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
+    if (count == 0 || in_len == 0) {
+        if (res_dev) {
+            mvbk::set_result_kernel<<<1, 1, 0, stream>>>(res_dev, count == 0 ? MVB_OK : MVB_TRUNCATED, 0, 0);
+            if (cudaGetLastError() != cudaSuccess) return MVB_ERR_CUDA;
+        }
+        return 0;
+    }
+    if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
+    Params p = {};
+    p.in = in;
+    p.mis = static_cast<long long>(reinterpret_cast<uintptr_t>(in) & 15u);
+    p.len = static_cast<long long>(in_len);  // (the totals pass covered all of in)
+    p.count = count;
+    p.out = out;
+    p.prev = prev;
+    p.prev_dev = prev_dev;
+    p.hdr = static_cast<WsHeader*>(ws);
+    p.res_dev = res_dev;
+    return launch_fused<true>(p, ws, ws_bytes, stream, 2, nullptr);
 }
 
 // Device buffers behind the synchronous host drop-ins, cached per thread.
@@ -903,24 +958,152 @@ int mvb_decode_delta_stream(const uint8_t* in, size_t in_len, size_t count, uint
     return decode_host(in, in_len, count, true, prev, out, mode, res);
 }
 
-int mvb_scan_totals_device(const uint8_t* in, size_t in_len, unsigned long long* count_dev, uint32_t* sum_dev,
-                           mvb_stream_t stream) {
-    if ((in == nullptr && in_len > 0) || count_dev == nullptr || sum_dev == nullptr) return MVB_ERR_INVALID_ARG;
-    if (cudaMemsetAsync(count_dev, 0, sizeof(unsigned long long), stream) != cudaSuccess ||
-        cudaMemsetAsync(sum_dev, 0, sizeof(uint32_t), stream) != cudaSuccess)
-        return MVB_ERR_CUDA;
-    if (in_len == 0) return 0;
-    const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
-    const size_t tiles = tiles_for(mis, in_len);
-    if (tiles >= (1ull << 32)) return MVB_ERR_INVALID_ARG;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, static_cast<size_t>(sms) * 8));
-    mvbk::vbyte_totals_kernel<<<grid, mvbk::kThreads, 0, stream>>>(in, static_cast<long long>(mis),
-                                                                   static_cast<long long>(in_len),
-                                                                   static_cast<unsigned>(tiles), count_dev, sum_dev);
-    return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+int mvb_delta_totals_device(const uint8_t* in, size_t in_len, unsigned long long* rec_dev, void* ws,
+                            size_t ws_bytes, mvb_stream_t stream) {
+    return delta_totals_device(in, in_len, rec_dev, ws, ws_bytes, stream);
+}
+
+int mvb_decode_delta_totaled_device(const uint8_t* in, size_t in_len, size_t count, uint32_t prev,
+                                    const uint32_t* prev_dev, uint32_t* out, mvb_result* res_dev, void* ws,
+                                    size_t ws_bytes, mvb_stream_t stream) {
+    return delta_totaled_device(in, in_len, count, prev, prev_dev, out, res_dev, ws, ws_bytes, stream);
+}
+
+int mvb_shard_cuts(const uint8_t* in, size_t in_len, int n, unsigned long long* cuts) {
+    if (n < 1 || cuts == nullptr || (in == nullptr && in_len > 0)) return MVB_ERR_INVALID_ARG;
+    cuts[0] = 0;
+    cuts[n] = in_len;
+    for (int g = 1; g < n; ++g) {
+        // the first integer start at or after the even cut (a byte whose
+        // predecessor terminates an integer); a continuation run with no end
+        // stays whole in the shard before
+        size_t p = static_cast<size_t>((static_cast<unsigned __int128>(in_len) * g) / n);
+        if (p < cuts[g - 1]) p = cuts[g - 1];
+        while (p < in_len && p > 0 && in[p - 1] >= 0x80u) ++p;
+        cuts[g] = p;
+    }
+    return 0;
+}
+
+}  // extern "C"
+
+namespace {
+// Per (device, shard slot) state of mvb_decode_delta_sharded: stream, workspace,
+// the shard's totals record, its DecodeResult.
+struct ShardCtx {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    void* ws = nullptr;
+    size_t ws_cap = 0;
+    unsigned long long* rec = nullptr;  // [count, sum]
+    mvb_result* res = nullptr;
+};
+std::mutex g_shard_mu;
+std::deque<ShardCtx> g_shards;  // (stable references: slots only ever grow at the end)
+
+int shard_ctx(int slot, int dev, size_t in_len, ShardCtx*& out) {
+    std::lock_guard<std::mutex> lk(g_shard_mu);
+    if (static_cast<int>(g_shards.size()) <= slot) g_shards.resize(slot + 1);
+    ShardCtx& c = g_shards[slot];
+    if (cudaSetDevice(dev) != cudaSuccess) return MVB_ERR_CUDA;
+    if (c.dev != dev) {  // (a slot moved to another device: start over)
+        c = ShardCtx();
+        c.dev = dev;
+        if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&c.rec), 16) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&c.res), sizeof(mvb_result)) != cudaSuccess)
+            return MVB_ERR_CUDA;
+    }
+    const size_t need = mvb_workspace_bytes(in_len);
+    if (need > c.ws_cap) {
+        if (c.ws && (cudaStreamSynchronize(c.stream) != cudaSuccess || cudaFree(c.ws) != cudaSuccess)) return MVB_ERR_CUDA;
+        c.ws = nullptr;
+        c.ws_cap = 0;
+        if (cudaMalloc(&c.ws, need) != cudaSuccess) return MVB_ERR_CUDA;
+        if (mvb_workspace_init(c.ws, need, c.stream) != 0 || cudaStreamSynchronize(c.stream) != cudaSuccess)
+            return MVB_ERR_CUDA;
+        c.ws_cap = need;
+    }
+    out = &c;
+    return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int mvb_decode_delta_sharded(int n, const int* devices, const uint8_t* const* shard_in, const size_t* shard_len,
+                             size_t count, uint32_t prev, uint32_t* const* shard_out, unsigned long long* offsets,
+                             mvb_result* res) {
+    if (n < 1 || devices == nullptr || shard_in == nullptr || shard_len == nullptr || shard_out == nullptr)
+        return MVB_ERR_INVALID_ARG;
+    int dev0 = 0;
+    if (cudaGetDevice(&dev0) != cudaSuccess) return MVB_ERR_CUDA;
+    std::vector<ShardCtx*> C(n);
+    for (int g = 0; g < n; ++g) {
+        const int rc = shard_ctx(g, devices[g], shard_len[g], C[g]);
+        if (rc) return rc;
+    }
+    // 1. totals of every shard but the last (one read of its bytes each), on
+    //    each shard's own stream and device, concurrently
+    std::vector<unsigned long long> rec(2 * n, 0);
+    for (int g = 0; g + 1 < n; ++g) {
+        if (cudaSetDevice(devices[g]) != cudaSuccess) return MVB_ERR_CUDA;
+        int rc = delta_totals_device(shard_in[g], shard_len[g], C[g]->rec, C[g]->ws, C[g]->ws_cap, C[g]->stream);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(&rec[2 * g], C[g]->rec, 16, cudaMemcpyDeviceToHost, C[g]->stream) != cudaSuccess)
+            return MVB_ERR_CUDA;
+    }
+    // 2. the exchange: 16 bytes per shard, through the host
+    for (int g = 0; g + 1 < n; ++g)
+        if (cudaSetDevice(devices[g]) != cudaSuccess || cudaStreamSynchronize(C[g]->stream) != cudaSuccess)
+            return MVB_ERR_CUDA;
+    // 3. every shard decodes its part of the first `count` integers from its carry
+    std::vector<unsigned long long> off(n, 0), want(n, 0), byte0(n, 0);
+    uint32_t carry = prev;
+    for (int g = 0; g < n; ++g) {
+        if (g) {
+            off[g] = off[g - 1] + rec[2 * (g - 1)];
+            byte0[g] = byte0[g - 1] + shard_len[g - 1];
+            carry += static_cast<uint32_t>(rec[2 * (g - 1) + 1]);
+        }
+        const unsigned long long room = count > off[g] ? count - off[g] : 0ull;
+        want[g] = (g + 1 < n) ? std::min<unsigned long long>(room, rec[2 * g]) : room;
+        if (offsets) offsets[g] = off[g];
+        if (cudaSetDevice(devices[g]) != cudaSuccess) return MVB_ERR_CUDA;
+        int rc;
+        if (g + 1 < n)
+            rc = delta_totaled_device(shard_in[g], shard_len[g], static_cast<size_t>(want[g]), carry, nullptr,
+                                      shard_out[g], C[g]->res, C[g]->ws, C[g]->ws_cap, C[g]->stream);
+        else
+            rc = decode_device(shard_in[g], shard_len[g], static_cast<size_t>(want[g]), true, carry, shard_out[g],
+                               MVB_STRICT, C[g]->res, C[g]->ws, C[g]->ws_cap, C[g]->stream);
+        if (rc) return rc;
+    }
+    // 4. the whole-stream DecodeResult: the first shard that is not OK decides
+    std::vector<mvb_result> r(n);
+    for (int g = 0; g < n; ++g) {
+        if (cudaSetDevice(devices[g]) != cudaSuccess ||
+            cudaMemcpyAsync(&r[g], C[g]->res, sizeof(mvb_result), cudaMemcpyDeviceToHost, C[g]->stream) != cudaSuccess ||
+            cudaStreamSynchronize(C[g]->stream) != cudaSuccess)
+            return MVB_ERR_CUDA;
+    }
+    cudaSetDevice(dev0);
+    mvb_result out = {};
+    out.status = MVB_TRUNCATED;
+    for (int g = 0; g < n; ++g) {
+        const bool last = g + 1 == n || off[g] + want[g] >= count;
+        if (r[g].status != MVB_OK || last) {
+            out.status = r[g].status;
+            out.values_written = off[g] + r[g].values_written;
+            out.bytes_consumed = byte0[g] + r[g].bytes_consumed;
+            if (r[g].status == MVB_TRUNCATED && r[g].values_written == 0 && g > 0 && want[g] > 0 &&
+                r[g].bytes_consumed == 0)
+                out.bytes_consumed = byte0[g];  // (nothing decodable in this shard: the end of the one before)
+            break;
+        }
+    }
+    if (res) *res = out;
+    return out.status;
 }
 
 size_t mvb_encoded_size(uint32_t x) { return vb_size(x); }

@@ -9,13 +9,17 @@ Each rank
    its cut (the first byte whose predecessor terminates an integer; in
    canonical data at most 4 bytes after the cut) and ends where the next
    rank's shard starts -- every integer is owned by exactly one shard;
-2. runs the pre-pass over its shard: integer count and, for delta decode,
-   the sum of its gaps mod 2^32 (``mvb_scan_totals_device``);
+2. runs the totals pass over its shard (delta decode, every rank but the
+   last): integer count and the sum of its gaps mod 2^32, one read of the
+   shard (``mvb_delta_totals_device``, last unit first so that the decode
+   pass finds the shard's head in L2);
 3. exchanges one small record per rank (start, end, count, sum) with a
    single all-gather -- the only collective; the bulk data never moves;
 4. decodes its shard as a standalone stream with ``count`` = its integers and
    ``prev`` = the caller's prev plus the gap sums of all earlier shards, into
-   its local output (global offset = integers in earlier shards).
+   its local output (global offset = integers in earlier shards): ranks that
+   ran the totals pass decode with it (``mvb_decode_delta_totaled_device``),
+   the last rank in one pass (totals and decode interleaved).
 
 The per-rank result is the reference's DecodeResult for the shard; the global
 result is assembled by ``combine_results`` exactly as decode_delta_scalar
@@ -170,24 +174,24 @@ class CudaShardOps(ShardOps):
         self.device = torch.device(device)
         self.lib = _lib.lib()
         self.dec = mvb.Decoder(self.device)
-        self.cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
-        self.sum = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.rec = torch.zeros(2, dtype=torch.int64, device=self.device)  # [count, gap sum]
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
 
     def totals_async(self, shard):
-        """Queue the pre-pass; returns device tensors (count, sum) without syncing."""
+        """Queue the totals pass; returns the device record [count, gap sum] without syncing."""
         n = shard.numel()
-        rc = self.lib.mvb_scan_totals_device(shard.data_ptr() if n else None, n, self.cnt.data_ptr(),
-                                             self.sum.data_ptr(), self._stream())
+        self.dec._ensure(max(n, 1))
+        rc = self.lib.mvb_delta_totals_device(shard.data_ptr() if n else None, n, self.rec.data_ptr(),
+                                              self.dec.ws.data_ptr(), self.dec.ws_bytes, self._stream())
         if rc != 0:
-            raise RuntimeError(f"mvb_scan_totals_device failed ({rc})")
-        return self.cnt, self.sum
+            raise RuntimeError(f"mvb_delta_totals_device failed ({rc})")
+        return self.rec
 
     def totals(self, shard) -> Tuple[int, int]:
-        c, s = self.totals_async(shard)
-        return int(c.item()), int(s.item()) & 0xFFFFFFFF
+        r = self.totals_async(shard).cpu().tolist()
+        return int(r[0]), int(r[1]) & 0xFFFFFFFF
 
     def decode(self, shard, count: int, prev: int, delta: bool, out=None):
         torch = self.torch
@@ -307,14 +311,17 @@ class DeviceShard:
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
 
     def prepass(self):
-        """Totals of this shard into the local record (delta, not the last rank)."""
+        """Totals of this shard into the local record (delta, not the last rank):
+        one read of the shard, last unit first; the workspace keeps the per-unit
+        totals for decode()."""
         if not self.delta or self.world == 1 or self.rank == self.world - 1:
             return
         n = self.bound
-        rc = self.lib.mvb_scan_totals_device(self.shard.data_ptr() if n else None, n, self.rec.data_ptr(),
-                                             self.rec.data_ptr() + 8, self._stream())
+        self.dec._ensure(max(n, 1))
+        rc = self.lib.mvb_delta_totals_device(self.shard.data_ptr() if n else None, n, self.rec.data_ptr(),
+                                              self.dec.ws.data_ptr(), self.dec.ws_bytes, self._stream())
         if rc != 0:
-            raise RuntimeError(f"mvb_scan_totals_device failed ({rc})")
+            raise RuntimeError(f"mvb_delta_totals_device failed ({rc})")
 
     def exchange(self):
         """All-gather of the records (the only collective)."""
@@ -334,9 +341,16 @@ class DeviceShard:
                                                  self.prev, self.carry.data_ptr(), None, s)
             if rc != 0:
                 raise RuntimeError(f"mvb_shard_carry_device failed ({rc})")
-            rc = self.lib.mvb_decode_delta_device_dprev(self.shard.data_ptr() if n else None, n, n,
-                                                        self.carry.data_ptr(), self.out.data_ptr() if n else None,
-                                                        0, self.dec.res.data_ptr(), ws, wsb, s)
+            if self.rank < self.world - 1:  # after this pass's totals pass (prepass)
+                rc = self.lib.mvb_decode_delta_totaled_device(self.shard.data_ptr() if n else None, n, n, 0,
+                                                              self.carry.data_ptr(),
+                                                              self.out.data_ptr() if n else None,
+                                                              self.dec.res.data_ptr(), ws, wsb, s)
+            else:
+                rc = self.lib.mvb_decode_delta_device_dprev(self.shard.data_ptr() if n else None, n, n,
+                                                            self.carry.data_ptr(),
+                                                            self.out.data_ptr() if n else None,
+                                                            0, self.dec.res.data_ptr(), ws, wsb, s)
         elif self.delta:
             rc = self.lib.mvb_decode_delta_device(self.shard.data_ptr() if n else None, n, n, self.prev,
                                                   self.out.data_ptr() if n else None, 0, self.dec.res.data_ptr(),

@@ -3,8 +3,9 @@
 CPU: the host logic (cuts, resync, per-shard counts, result combination) runs
 for W ranks against the oracle -- in-process with a threaded all-gather for
 many edge cases, and across real processes over a `gloo` group.  GPU: the
-pre-pass kernel (mvb_scan_totals_device) against the oracle, and W virtual
-shards decoded by the CUDA kernels on one device.  Every result must equal the
+totals pass (mvb_delta_totals_device) against the oracle, W virtual shards
+decoded by the CUDA kernels on one device through the Python shard logic, and
+the C-ABI multi-GPU entry (mvb_decode_delta_sharded) over W virtual GPUs.  Every result must equal the
 whole-stream oracle decode bit for bit (values and DecodeResult).
 """
 import os
@@ -252,8 +253,25 @@ def test_gloo_world2(tmp_path, world):
 
 # ----------------------------------------------------------------------- GPU
 
+def byte_weight_sum(seg) -> int:
+    """The totals pass's sum of a byte range starting at an integer boundary:
+    every byte's 7-bit digit times 128^(continuation bytes right before it in
+    its integer), mod 2^32 -- the values of the integers ending in the range
+    plus the partial value of an integer running past its end."""
+    b = np.asarray(seg, np.int64)
+    n = b.size
+    if n == 0:
+        return 0
+    idx = np.arange(n)
+    last = np.maximum.accumulate(np.where(b < 0x80, idx, -1))
+    prev_term = np.concatenate([[-1], last[:-1]])
+    run = idx - prev_term - 1
+    w = np.where(run < 5, np.left_shift(1, 7 * np.minimum(run, 4)), 0)
+    return int(((b & 0x7F) * w).sum() & 0xFFFFFFFF)
+
+
 @pytest.mark.gpu
-def test_totals_kernel_matches_oracle(cuda):
+def test_totals_pass_matches_oracle(cuda):
     import torch
 
     ops = S.CudaShardOps(cuda)
@@ -267,13 +285,57 @@ def test_totals_kernel_matches_oracle(cuda):
             seg = enc[a:a + ln]
             n = int((seg < 0x80).sum())
             c, s = ops.totals(dev[64 + a:64 + a + seg.size])
-            _, vals = oracle().decode(seg, n, STRICT)
             assert c == n
-            assert s == int(vals.astype(np.uint64).sum() & 0xFFFFFFFF), (a, ln)
+            assert s == byte_weight_sum(seg), (a, ln)
+            if seg.size and seg[-1] < 0x80:  # ends at an integer boundary: the value sum
+                _, vals = oracle().decode(seg, n, STRICT)
+                assert s == int(vals.astype(np.uint64).sum() & 0xFFFFFFFF)
     # count is the terminator count on arbitrary bytes too
     junk = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
     c, _ = ops.totals(torch.from_numpy(junk).to(cuda)[3:])
     assert c == int((junk[3:] < 0x80).sum())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+def test_c_abi_sharded_over_virtual_gpus(cuda, n):
+    """mvb_decode_delta_sharded: the whole stream's decode_delta_stream result
+    and values from n shards (all on device 0), including count limits,
+    truncation, malformed runs and prev wrap-around."""
+    import ctypes
+
+    import torch
+
+    from paper_1503_07387_b200 import _lib
+
+    L = _lib.lib()
+    gaps = W.mixture(400000, 91, 0.3, (1, 127), (128, 70000))
+    enc = oracle().encode_sequence(gaps)
+    bad = enc.copy()
+    bad[200001:200007] = 0x80  # a 7-byte run: malformed
+    cases = [(enc, gaps.size, 7), (enc, 123457, 0), (enc[:-1], gaps.size, 0xFFFFFFF0), (bad, gaps.size, 3),
+             (enc, gaps.size + 10, 5), (enc[:9], 5, 1)]
+    for data, count, prev in cases:
+        data = np.ascontiguousarray(data)
+        cuts = np.zeros(n + 1, np.uint64)
+        assert L.mvb_shard_cuts(data.ctypes.data, data.size, n, cuts.ctypes.data) == 0
+        ins = [torch.from_numpy(data[int(cuts[g]):int(cuts[g + 1])].copy()).to(cuda) for g in range(n)]
+        outs = [torch.full((max(x.numel(), 1),), -1, dtype=torch.int32, device=cuda) for x in ins]
+        devs = (ctypes.c_int * n)(*([cuda.index or 0] * n))
+        in_p = (ctypes.c_void_p * n)(*[x.data_ptr() if x.numel() else None for x in ins])
+        lens = (ctypes.c_size_t * n)(*[x.numel() for x in ins])
+        out_p = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+        offs = np.zeros(n, np.uint64)
+        res = _lib.MvbResult()
+        rc = L.mvb_decode_delta_sharded(n, devs, in_p, lens, count, prev, out_p, offs.ctypes.data, ctypes.byref(res))
+        ro, oo = oracle().decode_delta(data, count, prev)
+        assert rc == ro[0] and (res.status, res.values_written, res.bytes_consumed) == tuple(ro), (n, count, rc, ro)
+        for g in range(n):
+            a = int(offs[g])
+            b = min(int(offs[g + 1]) if g + 1 < n else ro[1], ro[1])
+            if b > a:
+                got = outs[g][:b - a].cpu().numpy().view(np.uint32)
+                assert np.array_equal(got, oo[a:b]), (n, count, g)
 
 
 @pytest.mark.gpu
