@@ -66,6 +66,22 @@ def build_workload(force: bool = False, verbose: bool = True) -> str:
     return target
 
 
+def build_cpp_tests(force: bool = False, verbose: bool = True) -> str:
+    """tests/cpp/sharded_abi_test: C++ driver of the multi-GPU C-ABI entry,
+    checked against the test-only oracle (needs libmvb_cuda.so and
+    oracle/liboracle.so)."""
+    src = os.path.join(ROOT, "tests", "cpp", "sharded_abi_test.cpp")
+    target = os.path.join(ROOT, "tests", "cpp", "sharded_abi_test")
+    deps = [src, os.path.join(HERE, "libmvb_cuda.so"), os.path.join(ROOT, "include", "mvb_cuda.h")]
+    if force or _stale(target, deps):
+        cuda = os.path.dirname(os.path.dirname(_nvcc()))
+        _run([os.environ.get("CXX", "g++"), "-O2", "-std=c++17", f"-I{cuda}/include", "-o", target, src,
+              f"-L{HERE}", "-lmvb_cuda", f"-L{os.path.join(ROOT, 'oracle')}", "-loracle", f"-L{cuda}/lib64", "-lcudart",
+              "-Wl,-rpath,$ORIGIN/../../paper_1503_07387_b200", "-Wl,-rpath,$ORIGIN/../../oracle",
+              f"-Wl,-rpath,{cuda}/lib64"], verbose)
+    return target
+
+
 def build_all(force: bool = False, verbose: bool = True) -> None:
     build_cuda(force, verbose)
     build_workload(force, verbose)

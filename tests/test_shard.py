@@ -406,3 +406,18 @@ def test_device_shards_equal_whole_stream(cuda, world):
             assert glob == tuple(want_r), (world, delta, glob, want_r)
             k = want_r[1]
             np.testing.assert_array_equal(got[:k], want[:k])
+
+
+@pytest.mark.gpu
+def test_cpp_driver_sharded_c_abi():
+    """The C++ caller of mvb_decode_delta_sharded (tests/cpp/sharded_abi_test.cpp):
+    1, 2, 3, 5 and 8 shards on this process's GPUs (repeated when there is one)
+    against the oracle -- plain, count-limited, truncated and malformed streams."""
+    import subprocess
+
+    from paper_1503_07387_b200 import build as B
+
+    exe = B.build_cpp_tests(verbose=False)
+    r = subprocess.run([exe, "400000", "1", "2", "3", "5", "8"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "25/25 sharded C-ABI cases passed" in r.stdout, r.stdout
