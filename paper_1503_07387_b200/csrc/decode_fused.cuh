@@ -401,6 +401,7 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     for (int k = 1; k < kNW; ++k) tot += tk[k];
     uint32_t acc = lane_scan_offset<true>(tot, carry);
     uint32_t sp = st_base + 4u * (a + incl - n_own);
+    MVB_CHECK(a + n_w <= static_cast<uint32_t>(kFStage));
 #pragma unroll
     for (int k = 0; k < kNW; ++k) {
         const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
@@ -413,6 +414,7 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
         slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc);
     }
     __syncwarp();
+    MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
     stage_out<false>(st_base, a, n_w, run, limit, out, lane);
     run += n_w;
     __syncwarp();  // the staging buffer is rewritten by the next slice
@@ -954,6 +956,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     auto load_unit = [&](long long u, int b) -> bool {  // TMA of unit u into buffer b (if inside the stream)
         const long long q = u * kUnit;
         const bool st = u < S.n_seg && q - 16 >= R.lo && q + kUnit <= R.hi;  // (warp-uniform)
+        MVB_CHECK(!st || (q - 16 >= R.lo && q + kUnit <= R.hi));
         if (st && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + q - 16, kUnit + 16, bar0 + 8u * b);
         return st;
     };
@@ -1035,6 +1038,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             uint32_t f_u = 0;
             const long long qu = u * kUnit;
             const bool u_staged = u < S.n_seg && qu - 16 >= R.lo && qu + kUnit <= R.hi;  // (warp-uniform)
+            MVB_CHECK(!u_staged || (qu - 16 >= R.lo && qu + kUnit <= R.hi));
             if (u_staged && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qu - 16, kUnit + 16, bar0 + 8u * b);
             // unit up's prefix entries: loads only (they were published long ago;
             // checked after unit u's publication, so a wait never delays it)

@@ -45,11 +45,23 @@
 // before each byte: a third lookback component (max) supplies it.
 #pragma once
 
+#include <cassert>
 #include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "../../include/mvb_cuda.h"
+// Debug builds (-DMVB_CHECKS=1, scripts/r2/gpu_checks.sh): device-side bounds
+// assertions on the staging stores, the output ranges and the unit loads (the
+// pool's compute-sanitizer is unavailable).
+#ifndef MVB_CHECKS
+#define MVB_CHECKS 0
+#endif
+#if MVB_CHECKS
+#define MVB_CHECK(c) assert(c)
+#else
+#define MVB_CHECK(c) ((void)0)
+#endif
 
 namespace mvbk {
 
@@ -85,7 +97,7 @@ constexpr unsigned long long ST_AGG = 1ull;
 constexpr unsigned long long ST_INCL = 2ull;
 
 struct alignas(16) WsHeader {
-    unsigned long long ticket;       // unused (tiles are indexed by blockIdx)
+    unsigned long long ticket;       // next tile / unit to hand out
     unsigned long long done;         // finished-CTA counter
     unsigned long long epoch;        // launches completed on this workspace
     unsigned long long err_idx_inv;  // max(~index) of strict-mode bad integer starts
@@ -561,9 +573,14 @@ __global__ void __launch_bounds__(kThreads, 5) vbyte_decode_kernel(Params P) {
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    // Tiles are indexed by blockIdx: CTAs are dispatched in index order, so
-    // every predecessor a lookback waits on is already resident.
-    const long long t = blockIdx.x;
+    // Tiles are handed out by an atomic ticket, not taken from blockIdx: the
+    // lookback of tile t waits on tiles < t, and a ticket is only ever held by
+    // a running CTA, so every tile waited on is resident whatever order the
+    // hardware dispatches CTAs in (finalize_launch resets the ticket).
+    __shared__ long long s_tile;
+    if (threadIdx.x == 0) s_tile = static_cast<long long>(atomicAdd(&P.hdr->ticket, 1ull));
+    __syncthreads();
+    const long long t = s_tile;
     const unsigned long long epoch = P.hdr->epoch + 1;  // constant during a launch
     if (tid == 0) {
         s_err = 0xFFFFFFFFu;

@@ -1219,6 +1219,10 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
     const uint32_t end = (static_cast<unsigned long long>(a + n) < room) ? a + n : static_cast<uint32_t>(room);
     uint32_t* const ob = out + g0;
     const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
+#if MVB_CHECKS
+    // every store of this copy-out lies in out[run, min(run + n, limit))
+    assert(a < 4u && end <= a + n && g0 + end <= limit && g0 + a == run);
+#endif
     if (lane < 8) {
         const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
         if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {

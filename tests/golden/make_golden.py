@@ -174,11 +174,67 @@ def main():
     if "--c4" in sys.argv:
         w = W.config4(); ck("config4", w.values, enc=w.encoded, delta=True, extra={"gen": "config4()"})
         del w
+    sums += extra_streams(ref, orc)
     with open(os.path.join(HERE, "checksums.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py (reference library oracle/_ref)",
                    "fnv": "FNV-1a 64 over bytes / little-endian u32 (tools/bench/runner.cpp:63-72)",
                    "streams": sums}, f, indent=1)
 
 
+def permissive_c1_bytes():
+    """config1's bytes with every 997th five-byte integer's fifth byte given
+    high bits (0x70: strict rejects it, permissive keeps its low 4 bits) and
+    every 50021st integer start overwritten by a 7-byte continuation run plus
+    a terminator (permissive splits it into 5-byte chunks)."""
+    w = W.config1()
+    b = w.encoded.copy()
+    term = np.flatnonzero(b < 0x80)
+    starts = np.concatenate([[0], term[:-1] + 1])
+    lens = term - starts + 1
+    five = term[lens == 5]
+    b[five[::997]] |= 0x70
+    for st in starts[1000::50021]:
+        if st + 8 < b.size:
+            b[st:st + 7] = 0x81 + np.arange(7, dtype=np.uint8)
+            b[st + 7] = 0x05
+    return b
+
+
+def extra_streams(ref, orc):
+    """Reference checksums of config3 (the batch: one decode_delta_stream per
+    list, runner.cpp:28-61) and of a full-size permissive stream."""
+    out = []
+    w = W.config3()
+    enc = np.ascontiguousarray(w.encoded)
+    bo = np.ascontiguousarray(w.byte_offsets.astype(np.uint64))
+    io = np.ascontiguousarray(w.int_offsets.astype(np.uint64))
+    vals = np.empty(w.count + 16, np.uint32)
+    bad = ref.decode_delta_lists(enc, bo, io, vals, 0, bo.size - 1)
+    out.append({"name": "config3", "delta": True, "prev": 0, "mode": STRICT, "count": int(w.count),
+                "lists": int(bo.size - 1), "in_len": int(enc.size), "in_fnv": orc.fnv_bytes(enc),
+                "offsets_fnv": orc.fnv_bytes(np.concatenate([bo.view(np.uint8), io.view(np.uint8)])),
+                "out_fnv": orc.fnv_u32(vals[: w.count]), "lists_not_ok": int(bad), "gen": "config3()"})
+    print("config3", enc.size, bad, flush=True)
+    b = permissive_c1_bytes()
+    for mode, tag in ((PERMISSIVE, "permissive"), (STRICT, "strict")):
+        r, o = ref.decode_scalar(b, b.size, mode)  # every integer there is (truncated at the end)
+        out.append({"name": f"config1_mutated_{tag}", "delta": False, "prev": 0, "mode": mode, "count": int(b.size),
+                    "in_len": int(b.size), "in_fnv": orc.fnv_bytes(b), "out_fnv": orc.fnv_u32(o[: r[1]]),
+                    "status": r[0], "values_written": r[1], "bytes_consumed": r[2],
+                    "gen": "permissive_c1_bytes() (tests/golden/make_golden.py)"})
+        print(f"config1_mutated_{tag}", b.size, r, flush=True)
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if "--extra-only" in sys.argv:  # append the extra streams to the existing checksums
+        path = os.path.join(HERE, "checksums.json")
+        with open(path) as f:
+            d = json.load(f)
+        extra = extra_streams(RefLib(), Oracle())
+        names = {e["name"] for e in extra}
+        d["streams"] = [e for e in d["streams"] if e["name"] not in names] + extra
+        with open(path, "w") as f:
+            json.dump(d, f, indent=1)
+    else:
+        main()

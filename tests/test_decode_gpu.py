@@ -1,6 +1,8 @@
 """Parity of the sm_100a decoder (through the C ABI) with the oracle and the
 reference's golden vectors.  Integer work: every comparison is bit-exact,
 including DecodeResult's status, values_written and bytes_consumed."""
+import os
+
 import numpy as np
 import pytest
 
@@ -263,6 +265,48 @@ def test_full_size_configs_checksums(name, golden, oracle):
     assert r == (s["status"], s["values_written"], s["bytes_consumed"])
     assert oracle.fnv_u32(out) == s["out_fnv"]
     assert np.array_equal(out, w.expected())
+
+
+@pytest.mark.parametrize("tag", ["permissive", "strict"])
+def test_full_size_permissive_stream(tag, golden, oracle):
+    """A full-size (config1, 50 MB) stream with non-canonical fifth bytes and
+    7-byte continuation runs: permissive mode splits and masks them exactly as
+    the reference does (decode_test.cpp:241-263 at size), strict mode stops at
+    the first one; pinned by the reference's own checksums."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("make_golden", os.path.join(os.path.dirname(__file__), "golden",
+                                                                              "make_golden.py"))
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    b = mg.permissive_c1_bytes()
+    _, sums = golden
+    s = sums[f"config1_mutated_{tag}"]
+    assert oracle.fnv_bytes(b) == s["in_fnv"]
+    r, out = gpu_decode(b, s["count"], s["mode"])
+    assert r == (s["status"], s["values_written"], s["bytes_consumed"])
+    assert oracle.fnv_u32(out[: r[1]]) == s["out_fnv"]
+
+
+def test_config3_batch_matches_reference_checksum(golden, oracle, cuda):
+    """The c3 batch (65,536 lists) in one batched launch against the
+    reference's per-list decode_delta_stream output (checksum)."""
+    import torch
+
+    _, sums = golden
+    s = sums["config3"]
+    w = W.config3()
+    assert oracle.fnv_bytes(w.encoded) == s["in_fnv"]
+    bo = w.byte_offsets.astype(np.uint64)
+    io = w.int_offsets.astype(np.uint64)
+    out = torch.empty(w.count, dtype=torch.int32, device=cuda)
+    res = torch.zeros(3 * (bo.size - 1), dtype=torch.int64, device=cuda)
+    d = mvb.Decoder(cuda, 1 << 12)
+    d.decode_lists(torch.from_numpy(w.encoded).to(cuda), torch.from_numpy(bo.view(np.int64)).to(cuda),
+                   torch.from_numpy(io.view(np.int64)).to(cuda), out, results=res, delta=True)
+    rr = res.cpu().numpy().reshape(-1, 3)
+    assert int((rr[:, 0] != 0).sum()) == s["lists_not_ok"]
+    assert oracle.fnv_u32(out.cpu().numpy().view(np.uint32)) == s["out_fnv"]
 
 
 def test_config4_full_size_device(golden, oracle, cuda):
