@@ -47,6 +47,9 @@ namespace mvbk {
 #ifndef MVB_F_UNIT
 #define MVB_F_UNIT 4096  // bytes per unit (a multiple of 1 KiB)
 #endif
+#ifndef MVB_BULK_OUT
+#define MVB_BULK_OUT 1  // copy-out of plain-layout staging by TMA bulk copies (0: ld.shared / st.global quads)
+#endif
 #ifndef MVB_F_BLOCKS
 #define MVB_F_BLOCKS 4  // resident CTAs per SM (shared memory: one unit buffer + staging per warp)
 #endif
@@ -358,7 +361,7 @@ __device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t 
 template <int kNW>
 __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, unsigned long long& run,
                                              uint32_t out_w, unsigned long long limit, uint32_t* out, uint32_t& carry,
-                                             int lane) {
+                                             int lane, unsigned long long pol) {
     constexpr int kStride = 4 * kNW - 1;
     const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
     // the lane's bytes [b0, b0 + kStride) and the 4 before them
@@ -402,6 +405,10 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     uint32_t acc = lane_scan_offset<true>(tot, carry);
     uint32_t sp = st_base + 4u * (a + incl - n_own);
     MVB_CHECK(a + n_w <= static_cast<uint32_t>(kFStage));
+#if MVB_BULK_OUT
+    stage_wait_read(lane);  // the previous slice's copy-out has read the staging buffer
+    __syncwarp();
+#endif
 #pragma unroll
     for (int k = 0; k < kNW; ++k) {
         const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
@@ -413,11 +420,19 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
         slot_store_w<false>(sp, w[k + 1], 0x800000u, o2);
         slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc);
     }
+#if MVB_BULK_OUT
+    stage_fence();
+    __syncwarp();
+    MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
+    stage_out_bulk(st_base, a, n_w, run, limit, out, lane, pol);
+    run += n_w;
+#else
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
     stage_out<false>(st_base, a, n_w, run, limit, out, lane);
     run += n_w;
     __syncwarp();  // the staging buffer is rewritten by the next slice
+#endif
 }
 
 // A delta unit staged in shared memory whose integers all have at most 3
@@ -426,14 +441,15 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
 // carry: every byte before the unit (the prefix tree's sums count bytes, so
 // no straddle correction); values go to out[base ...].
 __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, unsigned long long base, uint32_t carry,
-                                               unsigned long long limit, uint32_t* out, uint32_t* stage, int lane) {
+                                               unsigned long long limit, uint32_t* out, uint32_t* stage, int lane,
+                                               unsigned long long pol) {
     static_assert(kUnit == 3 * 992 + 1120, "the d3 slicing covers a 4 KiB unit");
     const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
     const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     unsigned long long run = base;
 #pragma unroll 1
-    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, run, out_w, limit, out, carry, lane);
-    slice_d3_odd<9>(ubuf, 2976u, st_base, run, out_w, limit, out, carry, lane);
+    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, run, out_w, limit, out, carry, lane, pol);
+    slice_d3_odd<9>(ubuf, 2976u, st_base, run, out_w, limit, out, carry, lane, pol);
 }
 
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
@@ -443,7 +459,7 @@ template <bool kDelta, bool kSwz>
 __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs, long long qe,
                                                 unsigned long long base, uint32_t carry, unsigned long long limit,
                                                 uint32_t* out, uint32_t* stage, uint32_t ubuf, int lane,
-                                                const RangeSink& K, RangeOut& ro) {
+                                                const RangeSink& K, RangeOut& ro, unsigned long long pol) {
     const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
     const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     const int ns = static_cast<int>((qe - qs + kLLSlice - 1) / kLLSlice);
@@ -544,6 +560,10 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
             F5 &= T32;
         }
         if (n_w) last_i = i;
+#if MVB_BULK_OUT
+        stage_wait_read(lane);  // an earlier copy-out (this unit's or the previous one's) has read the staging buffer
+        __syncwarp();
+#endif
         if (take3) {
             // carry: complete integers before the slice -> every byte before it
             const uint32_t hin = __shfl_sync(0xFFFFFFFFu, tail_value(wp3), 0);
@@ -568,6 +588,15 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
             carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
                                                st_base + 4u * (a + wexcl), st_base + kSparseWin + 72u * lane, carry);
         if (n_w == 0) continue;
+#if MVB_BULK_OUT
+        if (!kSwz) {
+            stage_fence();
+            __syncwarp();
+            stage_out_bulk(st_base, a, n_w, run, limit, out, lane, pol);
+            run += n_w;
+            continue;
+        }
+#endif
         __syncwarp();
         stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
         run += n_w;
@@ -910,6 +939,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
     const long long q_stream_end = (R.hi + 15) & ~15ll;
     const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
+    const unsigned long long pol = l2_evict_first();  // (output copies: written once, never read here)
     // the previous grid on the stream (e.g. the previous decode on this
     // workspace: it resets the ticket and advances the epoch) is complete and
     // visible after this
@@ -933,7 +963,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 // every integer has at most 3 bytes, integer count-1 ends after the
                 // unit: the dp2a path throughout (carry: every byte before the unit)
                 const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
-                decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane);
+                decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane, pol);
             } else {
                 uint32_t straddle = 0;
                 if (kDelta) {
@@ -946,10 +976,10 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 RangeOut ro;
                 if (swz)
                     decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
-                                                 ro);
+                                                 ro, pol);
                 else
                     decode_unit_ll<kDelta, false>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
-                                                  ro);
+                                                  ro, pol);
             }
         }
     };
@@ -1015,6 +1045,9 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             st = stn;
             b ^= 1;
         }
+#if MVB_BULK_OUT
+        stage_wait_all(lane);
+#endif
         fused_complete(F, tag);
         return;
     }
@@ -1073,6 +1106,9 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             c_up = c_u;
             f_up = f_u;
         }
+#if MVB_BULK_OUT
+        stage_wait_all(lane);
+#endif
     }
     fused_complete(F, tag);
 }

@@ -1256,6 +1256,54 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
     if (i + 256 < i1) __stcs(dst + 64, lds128(ae + off + 1024u));
 }
 
+// ---- copy-out by the TMA (plain staging layout only) ----
+//
+// stage_out's whole quads leave as one bulk copy shared -> global
+// (cp.async.bulk, issued by lane 0: no ld.shared / st.global instructions, no
+// address arithmetic); the <= 3 + 3 integers of the partial quads at both ends
+// by lanes 0..7 as before.  Protocol per staging buffer:
+//   writers    st.shared ...; stage_fence() (every lane: its generic-proxy
+//              writes become visible to the async proxy); __syncwarp()
+//   copy-out   stage_out_bulk() (lane 0 commits one bulk group)
+//   next use   stage_wait_read() (lane 0 waits until the TMA has read the
+//              buffer); __syncwarp(); st.shared ...
+// and stage_wait_all() before the warp's last instruction.
+__device__ __forceinline__ void stage_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void stage_wait_read(int lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait_all(int lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void stage_out_bulk(uint32_t st_base, uint32_t a, uint32_t n, unsigned long long run,
+                                               unsigned long long limit, uint32_t* out, int lane,
+                                               unsigned long long pol) {
+    if (run >= limit) return;
+    const unsigned long long g0 = run - a;
+    const unsigned long long room = limit - g0;
+    const uint32_t end = (static_cast<unsigned long long>(a + n) < room) ? a + n : static_cast<uint32_t>(room);
+    uint32_t* const ob = out + g0;
+    const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
+#if MVB_CHECKS
+    assert(a < 4u && end <= a + n && g0 + end <= limit && g0 + a == run);
+#endif
+    if (lane < 8) {
+        const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(st_base + 4u * i) : "memory");
+            __stcs(ob + i, v);
+        }
+    }
+    if (lane == 0) {
+        if (i1 > i0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(ob + i0),
+                         "r"(st_base + 4u * i0), "r"(4u * (i1 - i0)), "l"(pol)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
 
 // ring: shared-memory address of the warp's 2 x kLLSlice-byte input ring.
 // Slices (kLLSlice bytes: 32 per lane) are indexed from qs; interior slices
