@@ -50,6 +50,12 @@ namespace mvbk {
 #ifndef MVB_BULK_OUT
 #define MVB_BULK_OUT 1  // copy-out of plain-layout staging by TMA bulk copies (0: ld.shared / st.global quads)
 #endif
+#ifndef MVB_F_PF
+#define MVB_F_PF 8  // L2 prefetch distance of the unit loads, in eighths of a round of tickets (0: none)
+#endif
+#ifndef MVB_F_LATE
+#define MVB_F_LATE 0  // 1: a unit's prefix entries are checked (and waited for) after the next unit's publication
+#endif
 #ifndef MVB_F_BLOCKS
 #define MVB_F_BLOCKS 4  // resident CTAs per SM (shared memory: one unit buffer + staging per warp)
 #endif
@@ -73,7 +79,6 @@ struct FusedParams {
     SegParams S;                 // in, mis, len, count, out, prev, prev_dev, seg_bytes (= kUnit), n_seg, hdr, res_dev
     int swz;                     // staging swizzle: 0 never, 1 always, 2 dense units (debug switch)
     int narrow;                  // every count fits 32 bits (stream < 4 GiB): warp sums by redux
-    int early;                   // many units per warp: load a unit's prefix entries before the next unit's totals
     int mode;                    // 0 totals and decode, 1 totals only (-> rec), 2 decode only (totals of a mode-1 launch)
     unsigned long long* rec;     // mode 1: the stream's [integer count, value sum]
     int levels;                  // tree levels in use (32^levels >= n_seg)
@@ -358,12 +363,39 @@ __device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t 
 // first) is masked out as a digit-0 continuation byte.
 
 // One d3 slice at unit offset `off` (bytes) with lanes of 4 * kNW - 1 bytes.
+// Copy-out of a d3 slice: stage[a, a + n) -> op[0, n) with op - a 16-byte
+// aligned (a = the low bits of op).  The whole slice lies before the count
+// limit (decode_unit_d3's precondition), so nothing is clipped: the whole
+// quads leave as one bulk copy, the <= 3 + 3 integers of the partial quads by
+// lanes 0..7 (stage_out_bulk's protocol, without its 64-bit range arithmetic).
+__device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t a, uint32_t n, uint32_t* op, int lane,
+                                             unsigned long long pol) {
+    const uint32_t end = a + n;
+    const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
+    uint32_t* const ob = op - a;
+    if (lane < 8) {
+        const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+        if (lane < 4 ? (a != 0u && i >= a && i < end) : (i < end && i1 >= i0)) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(st_base + 4u * i) : "memory");
+            __stcs(ob + i, v);
+        }
+    }
+    if (lane == 0) {
+        if (i1 > i0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(ob + i0),
+                         "r"(st_base + 4u * i0), "r"(4u * (i1 - i0)), "l"(pol)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
+// op (in/out): the slice's first output, out + its index.
 template <int kNW>
-__device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, unsigned long long& run,
-                                             uint32_t out_w, unsigned long long limit, uint32_t* out, uint32_t& carry,
-                                             int lane, unsigned long long pol) {
+__device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, uint32_t*& op,
+                                             uint32_t& carry, int lane, unsigned long long pol) {
     constexpr int kStride = 4 * kNW - 1;
-    const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
+    const uint32_t a = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(op) >> 2) & 3u;  // staging offset of the slice
     // the lane's bytes [b0, b0 + kStride) and the 4 before them
     const uint32_t h0 = ubuf + off + static_cast<uint32_t>(kStride * lane) - 4u;
     const uint32_t sh = 8u * (h0 & 3u);
@@ -424,13 +456,13 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     stage_fence();
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    stage_out_bulk(st_base, a, n_w, run, limit, out, lane, pol);
-    run += n_w;
+    stage_out_d3(st_base, a, n_w, op, lane, pol);
+    op += n_w;
 #else
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    stage_out<false>(st_base, a, n_w, run, limit, out, lane);
-    run += n_w;
+    stage_out<false>(st_base, a, n_w, a, ~0ull, op - a, lane);
+    op += n_w;
     __syncwarp();  // the staging buffer is rewritten by the next slice
 #endif
 }
@@ -440,16 +472,13 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
 // every slice takes the dp2a path with no range masks, votes or limit checks.
 // carry: every byte before the unit (the prefix tree's sums count bytes, so
 // no straddle correction); values go to out[base ...].
-__device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, unsigned long long base, uint32_t carry,
-                                               unsigned long long limit, uint32_t* out, uint32_t* stage, int lane,
+// op: the unit's first output (out + its index).
+__device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, uint32_t* op, uint32_t carry, uint32_t st_base, int lane,
                                                unsigned long long pol) {
     static_assert(kUnit == 3 * 992 + 1120, "the d3 slicing covers a 4 KiB unit");
-    const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
-    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-    unsigned long long run = base;
 #pragma unroll 1
-    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, run, out_w, limit, out, carry, lane, pol);
-    slice_d3_odd<9>(ubuf, 2976u, st_base, run, out_w, limit, out, carry, lane, pol);
+    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, op, carry, lane, pol);
+    slice_d3_odd<9>(ubuf, 2976u, st_base, op, carry, lane, pol);
 }
 
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
@@ -642,23 +671,25 @@ __device__ __forceinline__ void fentry_get(const FEntry* e, unsigned tag, unsign
 
 // Publish entry i of level l (one lane) and aggregate upwards: the last
 // child to arrive at a parent sums the parent's children (the whole warp).
-__device__ __forceinline__ void fused_publish(const FusedParams& F, int l, long long i, unsigned long long cnt,
+__device__ __forceinline__ void fused_publish(const FusedParams& F, int l, uint32_t i, unsigned long long cnt,
                                               uint32_t sum, unsigned tag, int lane, uint32_t flags = 0u) {
     for (;;) {
         if (lane == 0) fentry_put(F.tree[l] + i, cnt, sum, tag, l == 0 ? flags : 0u);
         if (l + 1 >= F.levels) return;
-        const long long par = i >> 5;
-        const unsigned kids = static_cast<unsigned>((F.n_at[l] - (par << 5)) < 32 ? F.n_at[l] - (par << 5) : 32);
+        const uint32_t par = i >> 5;
+        const uint32_t left = static_cast<uint32_t>(F.n_at[l]) - (par << 5);  // children from the parent's first on
         unsigned last = 0;
         if (lane == 0) {
             const unsigned n = atomicAdd(F.arrive[l + 1] + par, 1u) + 1u;
-            last = (kids == 32u ? (n & 31u) : n % kids) == 0u ? 1u : 0u;
+            if (left >= 32u) last = (n & 31u) == 0u ? 1u : 0u;
+            else last = n % left == 0u ? 1u : 0u;  // (the level's last, partial parent)
         }
         last = __shfl_sync(0xFFFFFFFFu, last, 0);
         if (!last) return;
+        const uint32_t kids = left < 32u ? left : 32u;
         unsigned long long c = 0;
         uint32_t s = 0;
-        if (lane < kids) fentry_get(F.tree[l] + (par << 5) + lane, tag, c, s);
+        if (static_cast<uint32_t>(lane) < kids) fentry_get(F.tree[l] + ((par << 5) + lane), tag, c, s);
         sum = __reduce_add_sync(0xFFFFFFFFu, s);
         if (F.narrow) {
             cnt = __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(c));
@@ -746,48 +777,54 @@ __device__ __forceinline__ void unit_totals(uint32_t ubuf, int n_it, int lane, u
 
 // fused_prefix in two halves: the entries' loads are issued early (their
 // latency overlaps other work), the tags checked -- and stale entries
-// waited for -- later.
+// waited for -- later.  v < n_seg <= 32^levels, so v >> (5 * l) is 0 at the
+// levels not in use: they cost a shift and a compare.
 struct PrefixLoads {
     unsigned long long c[kFLevels], s[kFLevels];
 };
-__device__ __forceinline__ void fused_prefix_issue(const FusedParams& F, long long v, int lane, PrefixLoads& P) {
+__device__ __forceinline__ void fused_prefix_issue(const FusedParams& F, uint32_t v, int lane, PrefixLoads& P) {
 #pragma unroll
     for (int l = 0; l < kFLevels; ++l) {
-        P.c[l] = 0;
-        P.s[l] = 0;
-        if (l < F.levels && lane < ((v >> (5 * l)) & 31)) {
-            const FEntry* e = F.tree[l] + (((v >> (5 * l)) >> 5) << 5) + lane;
+        const uint32_t vl = v >> (5 * l);
+        if (static_cast<uint32_t>(lane) < (vl & 31u)) {
+            const FEntry* e = F.tree[l] + ((vl & ~31u) + static_cast<uint32_t>(lane));
             asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(P.c[l]), "=l"(P.s[l]) : "l"(e) : "memory");
         }
     }
 }
-__device__ __forceinline__ void fused_prefix_finish(const FusedParams& F, long long v, unsigned tag, int lane,
-                                                    PrefixLoads& P, unsigned long long& cnt, unsigned long long& sum) {
+template <bool kNarrow>
+__device__ __forceinline__ void fused_prefix_finish_n(const FusedParams& F, uint32_t v, unsigned tag, int lane,
+                                                      PrefixLoads& P, unsigned long long& cnt, uint32_t& sum) {
     unsigned long long c = 0;
-    uint32_t s = 0;
+    uint32_t c32 = 0, s = 0;
 #pragma unroll
     for (int l = 0; l < kFLevels; ++l) {
-        if (l < F.levels && lane < ((v >> (5 * l)) & 31)) {
-            unsigned long long ec;
-            uint32_t es;
-            if ((P.c[l] & 0xFFFFFFull) == tag && (P.s[l] & 0xFFFFFFull) == tag) {
-                ec = P.c[l] >> 24;
-                es = static_cast<uint32_t>(P.s[l] >> 32);
-            } else {
-                fentry_get(F.tree[l] + (((v >> (5 * l)) >> 5) << 5) + lane, tag, ec, es);
+        const uint32_t vl = v >> (5 * l);
+        if (static_cast<uint32_t>(lane) < (vl & 31u)) {
+            unsigned long long pc = P.c[l], ps = P.s[l];
+            while ((static_cast<uint32_t>(pc) & 0xFFFFFFu) != tag || (static_cast<uint32_t>(ps) & 0xFFFFFFu) != tag) {
+                __nanosleep(32);
+                const FEntry* e = F.tree[l] + ((vl & ~31u) + static_cast<uint32_t>(lane));
+                asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(pc), "=l"(ps) : "l"(e) : "memory");
             }
-            c += ec;
-            s += es;
+            if (kNarrow) c32 += static_cast<uint32_t>(pc >> 24);
+            else c += pc >> 24;
+            s += static_cast<uint32_t>(ps >> 32);
         }
     }
     sum = __reduce_add_sync(0xFFFFFFFFu, s);
-    if (F.narrow) {
-        cnt = __reduce_add_sync(0xFFFFFFFFu, static_cast<uint32_t>(c));
+    if (kNarrow) {
+        cnt = __reduce_add_sync(0xFFFFFFFFu, c32);
     } else {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
         cnt = c;
     }
+}
+__device__ __forceinline__ void fused_prefix_finish(const FusedParams& F, uint32_t v, unsigned tag, int lane,
+                                                    PrefixLoads& P, unsigned long long& cnt, uint32_t& sum) {
+    if (F.narrow) fused_prefix_finish_n<true>(F, v, tag, lane, P, cnt, sum);
+    else fused_prefix_finish_n<false>(F, v, tag, lane, P, cnt, sum);
 }
 
 // Completion (all threads of every CTA): the last CTA produces the DecodeResult.
@@ -950,21 +987,35 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(&S.hdr->epoch);
     const unsigned tag = static_cast<unsigned>(kMode == 2 ? epoch : epoch + 1ull) & 0xFFFFFFu;
     const uint32_t prev0 = kDelta ? (S.prev_dev ? S.prev + *S.prev_dev : S.prev) : 0u;
+    const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    // units [u_first, u_end) are staged in shared memory by the TMA: the unit and
+    // the 16 bytes before it lie inside the stream
+    const uint32_t u_first = static_cast<uint32_t>((R.lo + 16 + kUnit - 1) / kUnit);
+    const uint32_t u_end = static_cast<uint32_t>(R.hi / kUnit);
+    const uint32_t n_units = static_cast<uint32_t>(S.n_seg);
+    unsigned* const ticket = reinterpret_cast<unsigned*>(&S.hdr->ticket);  // (units < 2^28: the low word)
+#if MVB_F_PF
+    const uint32_t pf_dist = MVB_F_PF * gridDim.x * kSegWarps / 8u;
+#endif
+    // a delta unit whose integers all have at most 3 bytes (its totals pass's
+    // flags), staged, with integer count-1 ending after it: the dp2a path
+    auto unit_is_d3 = [&](uint32_t up, unsigned long long base, unsigned c_up, uint32_t f_up) -> bool {
+        return kDelta && up >= u_first && up < u_end && !(f_up & 1u) && base + c_up < S.count;
+    };
     // decode unit `up` (buffer bp), given its prefix and its totals pass's count / flags
-    auto decode_unit = [&](long long up, int bp, unsigned long long base, unsigned long long csum, unsigned c_up,
-                           uint32_t f_up) {
+    auto decode_unit = [&](uint32_t up, int bp, unsigned long long base, uint32_t csum, unsigned c_up, uint32_t f_up) {
         if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
-            const long long qs = up * kUnit;
+            const long long qs = static_cast<long long>(up) * kUnit;
             const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
-            const bool staged = qs - 16 >= R.lo && qs + kUnit <= R.hi;  // (warp-uniform)
+            const bool staged = up >= u_first && up < u_end;  // (warp-uniform)
             const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
-            const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
-            if (kDelta && staged && !(f_up & 1u) && base + c_up < S.count) {
-                // every integer has at most 3 bytes, integer count-1 ends after the
-                // unit: the dp2a path throughout (carry: every byte before the unit)
-                const uint32_t carry = static_cast<uint32_t>(csum) + prev0;
-                decode_unit_d3(ubuf, base, carry, S.count, S.out, stage, lane, pol);
+            if (unit_is_d3(up, base, c_up, f_up)) {
+                // (carry: every byte before the unit)
+                uint32_t carry = csum + prev0;
+                uint32_t* op = S.out + base;
+                decode_unit_d3(ubuf, op, carry, st_base, lane, pol);
             } else {
+                const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
                 uint32_t straddle = 0;
                 if (kDelta) {
                     uint32_t wb;
@@ -972,7 +1023,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                     else wb = r_word(R, qs - 4);
                     straddle = tail_value(wb);
                 }
-                const uint32_t carry = kDelta ? static_cast<uint32_t>(csum) - straddle + prev0 : 0u;
+                const uint32_t carry = kDelta ? csum - straddle + prev0 : 0u;
                 RangeOut ro;
                 if (swz)
                     decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
@@ -983,11 +1034,10 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             }
         }
     };
-    auto load_unit = [&](long long u, int b) -> bool {  // TMA of unit u into buffer b (if inside the stream)
-        const long long q = u * kUnit;
-        const bool st = u < S.n_seg && q - 16 >= R.lo && q + kUnit <= R.hi;  // (warp-uniform)
-        MVB_CHECK(!st || (q - 16 >= R.lo && q + kUnit <= R.hi));
-        if (st && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + q - 16, kUnit + 16, bar0 + 8u * b);
+    auto load_unit = [&](uint32_t u, int b) -> bool {  // TMA of unit u into buffer b (if inside the stream)
+        const bool st = u >= u_first && u < u_end;  // (warp-uniform)
+        if (st && lane == 0)
+            tma_bulk_load(buf0 + b * kUnitBuf, R.ab + static_cast<long long>(u) * kUnit - 16, kUnit + 16, bar0 + 8u * b);
         return st;
     };
     auto wait_unit = [&](int b) {
@@ -995,22 +1045,37 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         }
         phases ^= 1u << b;
     };
+    auto take_ticket = [&]() -> uint32_t {
+        unsigned t = 0;
+        if (lane == 0) {
+            t = atomicAdd(ticket, 1u);
+#if MVB_F_PF
+            // L2 prefetch of the unit about one round of tickets ahead (whichever warp
+            // takes it): its TMA load then finds the bytes in L2
+            const uint32_t v = (kMode == 1 ? n_units - 1u - t : t) + (kMode == 1 ? 0u - pf_dist : pf_dist);
+            if (v >= u_first && v < u_end)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(R.ab + static_cast<long long>(v) * kUnit),
+                             "r"(static_cast<uint32_t>(kUnit))
+                             : "memory");
+#endif
+        }
+        return __shfl_sync(0xFFFFFFFFu, t, 0);
+    };
     if constexpr (kMode == 1) {
         // totals only, last unit first: the decode pass that follows starts
         // with the units read last, still in L2
         for (;;) {
-            unsigned long long t = 0;
-            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
-            t = __shfl_sync(0xFFFFFFFFu, t, 0);
-            if (static_cast<long long>(t) >= S.n_seg) break;
-            const long long u = S.n_seg - 1 - static_cast<long long>(t);
+            const uint32_t t = take_ticket();
+            if (t >= n_units) break;
+            const uint32_t u = n_units - 1u - t;
             unsigned c_u;
             uint32_t su, f_u;
             if (load_unit(u, 0)) {
                 wait_unit(0);
                 unit_totals<kDelta>(buf0 + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
             } else {
-                fused_totals<kDelta>(S, u * kUnit, u * kUnit + kUnit, lane, c_u, su, 0u, &f_u);
+                const long long qs = static_cast<long long>(u) * kUnit;
+                fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
             }
             fused_publish(F, 0, u, c_u, su, tag, lane, f_u);
             __syncwarp();
@@ -1021,19 +1086,16 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     if constexpr (kMode == 2) {
         // decode only: every prefix is out; the next unit's bytes load while
         // this one is decoded
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
-        long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+        uint32_t u = take_ticket();
         int b = 0;
-        bool st = load_unit(u, b);
-        while (u < S.n_seg) {
-            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
-            const long long un = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
-            const bool stn = load_unit(un, b ^ 1);
+        bool st = u < n_units && load_unit(u, b);
+        while (u < n_units) {
+            const uint32_t un = take_ticket();
+            const bool stn = un < n_units && load_unit(un, b ^ 1);
             PrefixLoads P;
             fused_prefix_issue(F, u, lane, P);
-            unsigned long long base, csum, c_e;
-            uint32_t s_e;
+            unsigned long long base, c_e;
+            uint32_t csum, s_e;
             fused_prefix_finish(F, u, tag, lane, P, base, csum);
             const FEntry* e = F.tree[0] + u;
             fentry_get(e, tag, c_e, s_e);
@@ -1056,51 +1118,47 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         // decode the unit taken one iteration earlier (its predecessors took their
         // tickets before it and published right after, so its prefix is out).
         // The publication must follow the ticket closely: a unit is waited for by
-        // every later one.  (Taking the ticket before the previous unit's decode,
-        // to overlap the load with it, made later units wait a whole decode.)
-        long long up = -1;  // the unit awaiting its decode (buffer bp)
+        // every later one.  (Measured: decoding even one slice of the previous
+        // unit between the ticket and the totals, to hide the load's latency,
+        // made c4 four times slower -- the delays chain from unit to unit.)
+        bool have_up = false;
+        uint32_t up = 0;  // the unit awaiting its decode (buffer bp)
         int bp = 0;
         unsigned c_up = 0;  // its totals pass: integer count, flags
         uint32_t f_up = 0;
         for (;;) {
-            unsigned long long t = 0;
-            if (lane == 0) t = atomicAdd(&S.hdr->ticket, 1ull);
-            const long long u = static_cast<long long>(__shfl_sync(0xFFFFFFFFu, t, 0));
+            const uint32_t u = take_ticket();
             const int b = bp ^ 1;
             unsigned c_u = 0;
             uint32_t f_u = 0;
-            const long long qu = u * kUnit;
-            const bool u_staged = u < S.n_seg && qu - 16 >= R.lo && qu + kUnit <= R.hi;  // (warp-uniform)
-            MVB_CHECK(!u_staged || (qu - 16 >= R.lo && qu + kUnit <= R.hi));
-            if (u_staged && lane == 0) tma_bulk_load(buf0 + b * kUnitBuf, R.ab + qu - 16, kUnit + 16, bar0 + 8u * b);
-            // unit up's prefix entries: loads only (they were published long ago;
-            // checked after unit u's publication, so a wait never delays it)
+            const bool u_staged = u < n_units && load_unit(u, b);
+            // unit up's prefix entries (published about an iteration ago): the loads
+            // fly while unit u's bytes arrive
             PrefixLoads P;
-            if (up >= 0 && F.early) fused_prefix_issue(F, up, lane, P);
-            if (u < S.n_seg) {
-                const long long qs = qu;
-                const bool staged = u_staged;
+            unsigned long long base = 0;
+            uint32_t csum = 0;
+            if (have_up) {
+                fused_prefix_issue(F, up, lane, P);
+                if (!MVB_F_LATE) fused_prefix_finish(F, up, tag, lane, P, base, csum);
+            }
+            if (u < n_units) {
                 uint32_t su;
-                if (staged) {
-                    while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
-                    }
-                    phases ^= 1u << b;
+                if (u_staged) {
+                    wait_unit(b);
                     unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
                 } else {
+                    const long long qs = static_cast<long long>(u) * kUnit;
                     fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
                 }
                 fused_publish(F, 0, u, c_u, su, tag, lane, f_u);
             }
-            // ---- decode unit up (only now: a wait here must never hold back the
-            // publication of unit u, which later units wait for) ----
-            if (up >= 0) {
-                unsigned long long base, csum;
-                if (!F.early) fused_prefix_issue(F, up, lane, P);
-                fused_prefix_finish(F, up, tag, lane, P, base, csum);
+            if (have_up) {
+                if (MVB_F_LATE) fused_prefix_finish(F, up, tag, lane, P, base, csum);
                 decode_unit(up, bp, base, csum, c_up, f_up);
                 __syncwarp();  // (buffer bp is refilled next iteration)
             }
-            if (u >= S.n_seg) break;
+            if (u >= n_units) break;
+            have_up = true;
             up = u;
             bp = b;
             c_up = c_u;

@@ -328,8 +328,6 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
     S.res_dev = p.res_dev;
     F.swz = g_fused_swz;
     F.narrow = (p.mis + p.len) < (1ll << 32) ? 1 : 0;
-    // (a stream of few units per warp: the entries are rarely out that early)
-    F.early = f.n_seg >= 16 * f.W ? 1 : 0;
     F.mode = mode;
     F.rec = rec;
     F.levels = f.levels;
