@@ -363,19 +363,17 @@ __device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t 
 // first) is masked out as a digit-0 continuation byte.
 
 // One d3 slice at unit offset `off` (bytes) with lanes of 4 * kNW - 1 bytes.
-// Copy-out of a d3 slice: stage[a, a + n) -> op[0, n) with op - a 16-byte
-// aligned (a = the low bits of op).  The whole slice lies before the count
-// limit (decode_unit_d3's precondition), so nothing is clipped: the whole
-// quads leave as one bulk copy, the <= 3 + 3 integers of the partial quads by
-// lanes 0..7 (stage_out_bulk's protocol, without its 64-bit range arithmetic).
-__device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t a, uint32_t n, uint32_t* op, int lane,
+// Copy-out of a d3 slice: stage[first, end) -> ob[first, end) with ob 16-byte
+// aligned (stage[i] <-> ob[i]).  The whole slice lies before the count limit
+// (the d3 path's precondition), so nothing is clipped: the whole quads leave
+// as one bulk copy, the <= 3 + 3 integers of the partial quads by lanes 0..7
+// (stage_out_bulk's protocol, without its 64-bit range arithmetic).
+__device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t first, uint32_t end, uint32_t* ob, int lane,
                                              unsigned long long pol) {
-    const uint32_t end = a + n;
-    const uint32_t i0 = a ? 4u : 0u, i1 = end & ~3u;
-    uint32_t* const ob = op - a;
+    const uint32_t i0 = (first + 3u) & ~3u, i1 = end & ~3u;
     if (lane < 8) {
-        const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
-        if (lane < 4 ? (a != 0u && i >= a && i < end) : (i < end && i1 >= i0)) {
+        const uint32_t i = lane < 4 ? (first & ~3u) + static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+        if (lane < 4 ? (i >= first && i < i0 && i < end) : (i < end && i >= i0)) {
             uint32_t v;
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(st_base + 4u * i) : "memory");
             __stcs(ob + i, v);
@@ -391,9 +389,17 @@ __device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t a, uint3
 }
 
 // op (in/out): the slice's first output, out + its index.
-template <int kNW>
-__device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, uint32_t*& op,
-                                             uint32_t& carry, int lane, unsigned long long pol) {
+// kCheck (batched lists: no totals pass has looked at the bytes): the slice is
+// decoded only if no byte of it follows three continuation bytes and all its
+// integers end before `lim`; otherwise nothing is stored, op and carry stay,
+// and the result is false (the caller takes the general path from the slice
+// start).  skip: the slice's first `skip` integers are not stored (a list's
+// first slice: the <= 15 bytes before the list in its 16-byte-aligned unit
+// are zeroed in shared memory and decode as that many zeros).
+template <int kNW, bool kCheck = false>
+__device__ __forceinline__ bool slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, uint32_t*& op,
+                                             uint32_t& carry, int lane, unsigned long long pol, uint32_t skip = 0u,
+                                             const uint32_t* lim = nullptr) {
     constexpr int kStride = 4 * kNW - 1;
     const uint32_t a = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(op) >> 2) & 3u;  // staging offset of the slice
     // the lane's bytes [b0, b0 + kStride) and the 4 before them
@@ -410,12 +416,21 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     w[kNW] |= 0x80000000u;
     uint32_t W01[kNW], W23[kNW], w7[kNW], tk[kNW];
     uint32_t cp = w[0] & 0x80808080u, cc = 0;
+    // kCheck: bit 7 of a byte that ends a run of three continuation bytes
+    uint32_t run3 = kCheck ? (cp & (cp << 8) & (cp << 16)) : 0u;
 #pragma unroll
     for (int k = 0; k < kNW; ++k) {
         const uint32_t ck = w[k + 1] & 0x80808080u;
         cc = __dp4a(ck, 0x01010101u, cc);  // 128 per continuation byte
         // byte j: 1 if byte j-1 continues, 0x81 if bytes j-1 and j-2 do
-        const uint32_t x = __funnelshift_l(cp, ck, 1) | (__funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16));
+        uint32_t x;
+        if (kCheck) {
+            const uint32_t two = __funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16);
+            x = __funnelshift_l(cp, ck, 1) | two;
+            run3 |= (k == kNW - 1 ? ck & 0x00FFFFFFu : ck) & two;
+        } else {
+            x = __funnelshift_l(cp, ck, 1) | (__funnelshift_l(cp, ck, 8) & __funnelshift_l(cp, ck, 16));
+        }
         W01[k] = prmt_sign(x, 0u, 0x4140u) * 127u + 0x00010001u;
         W23[k] = prmt_sign(x, 0u, 0x4342u) * 127u + 0x00010001u;
         w7[k] = w[k + 1] ^ ck;
@@ -434,6 +449,40 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     uint32_t tot = tk[0];
 #pragma unroll
     for (int k = 1; k < kNW; ++k) tot += tk[k];
+    // kCheck, a slice with integers of 4 or 5 bytes: the weights above count a
+    // byte after three (four) continuation bytes as 2^14; a second dp2a chain
+    // adds the rest, (2^21 - 2^14) = 127 x 2^14 and (2^28 - 2^14) = 16383 x 2^14
+    // (16-bit weights 127 x {1, 129} from a byte code with bit 0 = three
+    // continuation bytes before, bit 7 = four).  The tables are rebuilt per
+    // word in both passes (lane total, outputs) instead of kept in registers.
+    bool lng = false;
+    auto long_word = [&](int k, uint32_t& B01, uint32_t& B23, uint32_t& bad) {
+        const uint32_t ck = w[k + 1] & 0x80808080u, cq = w[k] & 0x80808080u;
+        const uint32_t c3 = __funnelshift_l(cq, ck, 8) & __funnelshift_l(cq, ck, 16) & __funnelshift_l(cq, ck, 24);
+        const uint32_t c4 = c3 & cq;  // (byte j of the word before is byte j - 4)
+        const uint32_t xb = (c3 >> 7) | c4;
+        B01 = prmt_sign(xb, 0u, 0x4140u) * 127u;
+        B23 = prmt_sign(xb, 0u, 0x4342u) * 127u;
+        // strict mode: a fifth byte must be < 0x10 (internal.hpp:35)
+        const uint32_t x = w[k + 1];
+        const uint32_t hi4 = x | (x << 1) | (x << 2) | (x << 3);
+        bad |= c4 & hi4 & (k == kNW - 1 ? 0x00808080u : 0x80808080u);
+    };
+    if (kCheck) {
+        if (op + n_w >= lim) return false;
+        lng = __any_sync(0xFFFFFFFFu, (run3 & 0x80808080u) != 0u);
+        if (lng) {
+            uint32_t tb = 0, bad = 0;
+#pragma unroll
+            for (int k = 0; k < kNW; ++k) {
+                uint32_t B01, B23;
+                long_word(k, B01, B23, bad);
+                tb = dp2a_lo(B01, w7[k], dp2a_hi(B23, w7[k], tb));
+            }
+            if (__any_sync(0xFFFFFFFFu, bad != 0u)) return false;  // malformed: the general path reports it
+            tot += tb << 14;
+        }
+    }
     uint32_t acc = lane_scan_offset<true>(tot, carry);
     uint32_t sp = st_base + 4u * (a + incl - n_own);
     MVB_CHECK(a + n_w <= static_cast<uint32_t>(kFStage));
@@ -441,30 +490,53 @@ __device__ __forceinline__ void slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     stage_wait_read(lane);  // the previous slice's copy-out has read the staging buffer
     __syncwarp();
 #endif
+    if (kCheck && lng) {
+        uint32_t accb = 0;
 #pragma unroll
-    for (int k = 0; k < kNW; ++k) {
-        const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
-        const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
-        const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
-        acc += tk[k];
-        slot_store_w<false>(sp, w[k + 1], 0x80u, o0);
-        slot_store_w<false>(sp, w[k + 1], 0x8000u, o1);
-        slot_store_w<false>(sp, w[k + 1], 0x800000u, o2);
-        slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc);
+        for (int k = 0; k < kNW; ++k) {
+            uint32_t B01, B23, bad = 0;
+            long_word(k, B01, B23, bad);
+            const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
+            const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
+            const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
+            acc += tk[k];
+            const uint32_t b0 = dp2a_lo(B01 & 0xFFFFu, w7[k], accb);
+            const uint32_t b1 = dp2a_lo(B01, w7[k], accb);
+            const uint32_t b2 = dp2a_hi(B23 & 0xFFFFu, w7[k], b1);
+            accb = dp2a_hi(B23, w7[k], b1);
+            slot_store_w<false>(sp, w[k + 1], 0x80u, o0 + (b0 << 14));
+            slot_store_w<false>(sp, w[k + 1], 0x8000u, o1 + (b1 << 14));
+            slot_store_w<false>(sp, w[k + 1], 0x800000u, o2 + (b2 << 14));
+            slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc + (accb << 14));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kNW; ++k) {
+            const uint32_t o0 = dp2a_lo(W01[k] & 0xFFFFu, w7[k], acc);
+            const uint32_t o1 = dp2a_lo(W01[k], w7[k], acc);
+            const uint32_t o2 = dp2a_hi(W23[k] & 0xFFFFu, w7[k], o1);
+            acc += tk[k];
+            slot_store_w<false>(sp, w[k + 1], 0x80u, o0);
+            slot_store_w<false>(sp, w[k + 1], 0x8000u, o1);
+            slot_store_w<false>(sp, w[k + 1], 0x800000u, o2);
+            slot_store_w<false>(sp, w[k + 1], 0x80000000u, acc);
+        }
     }
 #if MVB_BULK_OUT
     stage_fence();
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    stage_out_d3(st_base, a, n_w, op, lane, pol);
+    stage_out_d3(st_base, a + skip, a + n_w, op - a, lane, pol);
     op += n_w;
 #else
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    stage_out<false>(st_base, a, n_w, a, ~0ull, op - a, lane);
+    if (n_w > skip) stage_out<false>(st_base + 4u * (skip & ~3u), (a + skip) & 3u, n_w - skip, (a + skip) & 3u, ~0ull,
+                                     op - a + (skip & ~3u) + ((a & 3u) + (skip & 3u) >= 4u ? 4 : 0), lane);
     op += n_w;
     __syncwarp();  // the staging buffer is rewritten by the next slice
 #endif
+    return true;
 }
 
 // A delta unit staged in shared memory whose integers all have at most 3
@@ -477,8 +549,8 @@ __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, uint32_t* op, uint
                                                unsigned long long pol) {
     static_assert(kUnit == 3 * 992 + 1120, "the d3 slicing covers a 4 KiB unit");
 #pragma unroll 1
-    for (int i = 0; i < 3; ++i) slice_d3_odd<8>(ubuf, 992u * i, st_base, op, carry, lane, pol);
-    slice_d3_odd<9>(ubuf, 2976u, st_base, op, carry, lane, pol);
+    for (int i = 0; i < 3; ++i) (void)slice_d3_odd<8>(ubuf, 992u * i, st_base, op, carry, lane, pol);
+    (void)slice_d3_odd<9>(ubuf, 2976u, st_base, op, carry, lane, pol);
 }
 
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
@@ -648,6 +720,7 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
     }
     ro.last_end = last_end;
     ro.n = run - base;
+    ro.carry = carry;
 }
 
 __device__ __forceinline__ void fentry_put(FEntry* e, unsigned long long cnt, uint32_t sum, unsigned tag,
@@ -973,7 +1046,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     }
     __syncwarp();
     uint32_t phases = 0;  // bit b: parity of buffer b's next completion
-    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
+    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len, S.mis, S.mis + S.len};
     const long long q_stream_end = (R.hi + 15) & ~15ll;
     const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
     const unsigned long long pol = l2_evict_first();  // (output copies: written once, never read here)

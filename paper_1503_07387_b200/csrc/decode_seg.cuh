@@ -443,9 +443,16 @@ __device__ __forceinline__ void seg_totals_run(const SegParams& S, long long it_
 // A byte range of a buffer in 16-byte-aligned coordinates: byte q lives at
 // ab[q]; bytes q < lo read as 0x00 (the range start is an integer boundary),
 // bytes q >= hi as 0x80 (no integer ends there).
+// x << n with PTX semantics (n >= 32 gives 0)
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, int n) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+    return r;
+}
 struct ByteRange {
     const uint8_t* ab;
     long long lo, hi;
+    long long elo, ehi;  // the caller's buffer (ab coordinates): bytes in [elo, ehi) may be read
 };
 __device__ __forceinline__ uint32_t r_byte(const ByteRange& R, long long q) {
     if (q < R.lo) return 0x00u;
@@ -456,8 +463,33 @@ __device__ __forceinline__ uint32_t r_word(const ByteRange& R, long long q) {
     return r_byte(R, q) | (r_byte(R, q + 1) << 8) | (r_byte(R, q + 2) << 16) | (r_byte(R, q + 3) << 24);
 }
 __device__ __forceinline__ bool r_inside(const ByteRange& R, long long q, long long n) { return q >= R.lo && q + n <= R.hi; }
+// Byte j of the result: 0xFF if j < n (n <= 0: none, n >= 4: all).
+__device__ __forceinline__ uint32_t low_bytes_mask(int n) {
+    const int k = n < 0 ? 0 : n > 4 ? 4 : n;
+    return ~shl_clamp(0xFFFFFFFFu, 8 * k);
+}
+// The 16 bytes at q (q a multiple of 16).  A block that straddles the range's
+// start or end but lies inside the caller's buffer (a list between its
+// neighbours in a batch) is one vector load masked in registers; only a block
+// that would touch bytes outside the buffer is assembled byte by byte.
 __device__ __forceinline__ uint4 r_load16(const ByteRange& R, long long q) {
     if (r_inside(R, q, 16)) return ldg_stream16(R.ab + q);
+    if (q + 16 <= R.lo) return make_uint4(0u, 0u, 0u, 0u);
+    if (q >= R.hi) return make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    if (q >= R.elo && q + 16 <= R.ehi) {
+        uint4 v = ldg_stream16(R.ab + q);
+        // bytes [nl, nh) of the block are inside the range (clamped to +-64)
+        const int nl = R.lo - q < -64 ? -64 : static_cast<int>(R.lo - q);
+        const int nh = R.hi - q > 64 ? 64 : static_cast<int>(R.hi - q);
+        uint32_t* const w = &v.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t below = low_bytes_mask(nl - 4 * k);   // bytes before the range: 0x00
+            const uint32_t inside = low_bytes_mask(nh - 4 * k);  // bytes past it: 0x80
+            (&v.x)[k] = (w[k] & ~below & inside) | (0x80808080u & ~inside);
+        }
+        return v;
+    }
     return make_uint4(r_word(R, q), r_word(R, q + 4), r_word(R, q + 8), r_word(R, q + 12));
 }
 __device__ __forceinline__ uint32_t r_inr16(const ByteRange& R, long long q0) {
@@ -515,6 +547,7 @@ __device__ __forceinline__ void slice_count_end(const ByteRange& R, const RangeS
 struct RangeOut {
     long long last_end;  // -1 if the range holds no integer
     unsigned long long n;
+    uint32_t carry;      // delta: the running value after the range's last integer
 };
 
 // ------------------------------------------------------------------ lane-local range decode
@@ -1467,6 +1500,7 @@ __device__ __forceinline__ void decode_range_ll(const ByteRange& R, long long qs
     }
     ro.last_end = last_end;
     ro.n = run - base;
+    ro.carry = carry;
 }
 
 // 16-byte-lane range decode (delta); ring: the warp's input ring (2 x 512 bytes used).  Slices
@@ -1600,6 +1634,7 @@ __device__ __forceinline__ void decode_range_ll16(const ByteRange& R, long long 
     }
     ro.last_end = last_end;
     ro.n = run - base;
+    ro.carry = carry;
 }
 
 // The lane-local range decode: 32-byte lanes (half the per-slice fixed work
@@ -1814,7 +1849,7 @@ __global__ void __launch_bounds__(kSegThreads, kDelta ? kLLBlocksD : kLLBlocks) 
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(vbase + 4 * kLaneStage));
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len};
+    const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len, S.mis, S.mis + S.len};
     // one contiguous run of segments per warp (the output index and carry after
     // segment s are those of s + 1, so only the run's first segment needs the
     // prefix)
@@ -1922,7 +1957,7 @@ __global__ void __launch_bounds__(kSegThreads, kDelta ? kLLBlocksD : kLLBlocks) 
             r.values_written = 0;
             r.bytes_consumed = 0;
         } else {
-            const ByteRange R = {L.ab, L.mis0 + b0, L.mis0 + b1};
+            const ByteRange R = {L.ab, L.mis0 + b0, L.mis0 + b1, L.mis0, L.mis0 + L.in_len};
             if (lane == 0) {
                 s_err_idx[wid] = ~0ull;
                 s_count_end[wid] = -1;

@@ -20,6 +20,7 @@
 #include "decode_kernel.cuh"
 #include "decode_seg.cuh"
 #include "decode_fused.cuh"
+#include "decode_lists.cuh"
 #include "totals_kernel.cuh"
 #include "encode_kernel.cuh"
 
@@ -783,10 +784,15 @@ int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byt
     if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;  // permissive lists: decode each list on its own
     if (ws == nullptr || ws_bytes < kHeaderBytes) return MVB_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(out) & 3u) return MVB_ERR_INVALID_ARG;
-    constexpr int kSmemB = mvbk::kLaneSmem;
+    // delta lists: the unit-based kernel (decode_lists.cuh); plain lists (and
+    // kernel choice 6, for comparisons): one range decode per list
+    const bool units = Delta && g_kernel_choice != 6;
+    const int kSmemB = units ? mvbk::kFSmem : mvbk::kLaneSmem;
     int sms = 0;
-    const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_lists_decode<Delta>), mvbk::kSegThreads,
-                                 kSmemB, &sms);
+    const int per_sm = units ? occupancy(reinterpret_cast<const void*>(mvbk::vbyte_lists_decode_units),
+                                         mvbk::kSegThreads, kSmemB, &sms)
+                             : occupancy(reinterpret_cast<const void*>(mvbk::vbyte_lists_decode<Delta>),
+                                         mvbk::kSegThreads, kSmemB, &sms);
     if (per_sm < 0) return MVB_ERR_CUDA;
     mvbk::ListParams L;
     const size_t mis = reinterpret_cast<uintptr_t>(in) & 15u;
@@ -804,7 +810,8 @@ int lists_device(const uint8_t* in, size_t in_len, const unsigned long long* byt
     const long long warps_needed = static_cast<long long>(n_lists);
     const long long ctas = std::min<long long>(static_cast<long long>(per_sm) * sms,
                                                (warps_needed + mvbk::kSegWarps - 1) / mvbk::kSegWarps);
-    mvbk::vbyte_lists_decode<Delta><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
+    if (units) mvbk::vbyte_lists_decode_units<<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
+    else mvbk::vbyte_lists_decode<Delta><<<static_cast<unsigned>(ctas), mvbk::kSegThreads, kSmemB, s>>>(L);
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
 // Batched host decode (mvb_decode_lists / mvb_decode_delta_lists): contiguous
