@@ -396,10 +396,17 @@ __device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t first, u
 // start).  skip: the slice's first `skip` integers are not stored (a list's
 // first slice: the <= 15 bytes before the list in its 16-byte-aligned unit
 // are zeroed in shared memory and decode as that many zeros).
+// A checked slice whose last integer is integer count-1 (op + its integers ==
+// lim) is decoded too; *end_off then receives the slice offset of the byte
+// after that integer (otherwise 0).  pad: the slice's last `pad` bytes lie
+// past the list's end and are zeroed in shared memory (a list's last slice):
+// they decode as that many integers after the real ones -- the first of them
+// may close an integer the list leaves unfinished -- which are not stored.
 template <int kNW, bool kCheck = false>
 __device__ __forceinline__ bool slice_d3_odd(uint32_t ubuf, uint32_t off, uint32_t st_base, uint32_t*& op,
                                              uint32_t& carry, int lane, unsigned long long pol, uint32_t skip = 0u,
-                                             const uint32_t* lim = nullptr) {
+                                             const uint32_t* lim = nullptr, uint32_t* end_off = nullptr,
+                                             uint32_t pad = 0u) {
     constexpr int kStride = 4 * kNW - 1;
     const uint32_t a = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(op) >> 2) & 3u;  // staging offset of the slice
     // the lane's bytes [b0, b0 + kStride) and the 4 before them
@@ -469,7 +476,20 @@ __device__ __forceinline__ bool slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
         bad |= c4 & hi4 & (k == kNW - 1 ? 0x00808080u : 0x80808080u);
     };
     if (kCheck) {
-        if (op + n_w >= lim) return false;
+        if (op + (n_w - pad) > lim) return false;
+        uint32_t eo = 0;
+        if (op + (n_w - pad) == lim) {
+            // the byte after the slice's last terminator (before the padding)
+            const int vl = static_cast<int>(kStride * 32 - pad) - kStride * lane;  // the lane's bytes before the padding
+            uint32_t e = 0;
+#pragma unroll
+            for (int k = 0; k < kNW; ++k) {
+                const uint32_t t = ~w[k + 1] & (k == kNW - 1 ? 0x00808080u : 0x80808080u) & low_bytes_mask(vl - 4 * k);
+                if (t) e = 4u * k + ((39u - __clz(t)) >> 3);
+            }
+            eo = __reduce_max_sync(0xFFFFFFFFu, e ? static_cast<uint32_t>(kStride * lane) + e : 0u);
+        }
+        *end_off = eo;
         lng = __any_sync(0xFFFFFFFFu, (run3 & 0x80808080u) != 0u);
         if (lng) {
             uint32_t tb = 0, bad = 0;
@@ -526,14 +546,15 @@ __device__ __forceinline__ bool slice_d3_odd(uint32_t ubuf, uint32_t off, uint32
     stage_fence();
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    stage_out_d3(st_base, a + skip, a + n_w, op - a, lane, pol);
-    op += n_w;
+    stage_out_d3(st_base, a + skip, a + n_w - pad, op - a, lane, pol);
+    op += n_w - pad;
 #else
     __syncwarp();
     MVB_CHECK(sp <= st_base + 4u * (a + incl));  // (each lane stored exactly its own integers)
-    if (n_w > skip) stage_out<false>(st_base + 4u * (skip & ~3u), (a + skip) & 3u, n_w - skip, (a + skip) & 3u, ~0ull,
-                                     op - a + (skip & ~3u) + ((a & 3u) + (skip & 3u) >= 4u ? 4 : 0), lane);
-    op += n_w;
+    if (n_w - pad > skip)
+        stage_out<false>(st_base + 4u * ((a + skip) & ~3u), (a + skip) & 3u, n_w - pad - skip, (a + skip) & 3u, ~0ull,
+                         op - a + ((a + skip) & ~3u), lane);
+    op += n_w - pad;
     __syncwarp();  // the staging buffer is rewritten by the next slice
 #endif
     return true;

@@ -100,8 +100,11 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
             const RangeSink K = {nullptr, &s_err_idx[wid], &s_err_pos[wid], &s_count_end[wid]};
             const unsigned long long limit = base + cnt;
             const long long U0 = R.lo & ~15ll;
-            const int n_sl = static_cast<int>((R.hi - U0) / 992);  // whole slices inside [U0, hi)
-            const int n_full = (n_sl + 3) / 4;                   // units of up to four slices
+            const long long span = R.hi - U0;
+            // slices (the last one may be partial); a list starting in the batch's first
+            // 16-byte block takes the general path (its first unit would start before `in`)
+            const int n_sl = R.hi > R.lo && U0 >= R.elo ? static_cast<int>((span + 991) / 992) : 0;
+            const int n_full = (n_sl + 3) / 4;                                        // units of up to four slices
             uint32_t carry = L.prev ? L.prev[l] : 0u;  // complete integers before (the general path's convention)
             unsigned long long run = base;             // the next output index
             long long last_end = -1;                   // the end of the last integer the general path saw
@@ -124,47 +127,79 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
             };
             if (n_full > 0) {
                 const uint32_t stray = static_cast<uint32_t>(R.lo - U0);
-                // unit 0 has no bytes before it to load (they are zeroed below)
-                if (lane == 0) tma_bulk_load(buf0 + 16u, R.ab + U0, 992u * static_cast<uint32_t>(n_sl < 4 ? n_sl : 4), bar0);
-                int loaded = 0, waited = -1;  // units whose load is issued / has landed
+                int loaded = -1, waited = -1;  // units whose load is issued / has landed
+                uint32_t tma_mask = 0;  // bit b: buffer b's unit has a bulk copy to wait for
+                uint32_t rem = 0;  // lane j: byte j of the loaded unit's last, partial 16-byte block
                 auto wait_load = [&](int b) {
-                    while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
+                    if ((tma_mask >> b) & 1u) {
+                        while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
+                        }
+                        phases ^= 1u << b;
                     }
-                    phases ^= 1u << b;
                 };
+                // unit k's bytes [u_lo, u_lo + ub): whole 16-byte blocks by one TMA bulk copy
+                // (with the 16 bytes before the unit, except unit 0: they are zeroed), the
+                // last ub % 16 bytes one per lane (the block may end outside the buffer)
+                auto unit_bytes = [&](int k) -> uint32_t {
+                    const long long left = span - static_cast<long long>(k) * kLUnit;
+                    return static_cast<uint32_t>(left < kLUnit ? left : kLUnit);
+                };
+                auto load_unit = [&](int k) {
+                    const int b = k & 1;
+                    const uint32_t ub = unit_bytes(k), tb = ub & ~15u;
+                    const uint8_t* src = R.ab + U0 + static_cast<long long>(k) * kLUnit;
+                    const bool tma = k > 0 || tb > 0;  // (warp-uniform; units after the first always load their 16 bytes before)
+                    tma_mask = (tma_mask & ~(1u << b)) | (tma ? 1u << b : 0u);
+                    if (tma && lane == 0) {
+                        if (k == 0) tma_bulk_load(buf0 + 16u, src, tb, bar0);
+                        else tma_bulk_load(buf0 + b * kUnitBuf, src - 16, tb + 16u, bar0 + 8u * b);
+                    }
+                    rem = static_cast<uint32_t>(lane) < ub - tb ? src[tb + lane] : 0u;
+                    loaded = k;
+                };
+                load_unit(0);
                 for (int k = 0; k < n_full && run < limit; ++k) {
                     const int b = k & 1;
-                    if (k + 1 < n_full) {
-                        if (lane == 0)
-                            tma_bulk_load(buf0 + (b ^ 1) * kUnitBuf,
-                                          R.ab + U0 + static_cast<long long>(k + 1) * kLUnit - 16,
-                                          992u * static_cast<uint32_t>(n_sl - 4 * (k + 1) < 4 ? n_sl - 4 * (k + 1) : 4) + 16u,
-                                          bar0 + 8u * (b ^ 1));
-                        loaded = k + 1;
-                    }
+                    const uint32_t ub = unit_bytes(k);
+                    const uint32_t ubuf = buf0 + b * kUnitBuf + 16u;
+                    const int sl = n_sl - 4 * k < 4 ? n_sl - 4 * k : 4;  // this unit's slices
                     wait_load(b);
                     waited = k;
-                    const uint32_t ubuf = buf0 + b * kUnitBuf + 16u;
+                    if (ub < 992u * sl) {
+                        // the last slice is partial: the bytes from the list's end on are
+                        // zeroed (the slice drops the integers they decode as)
+                        if (lane < 16) asm volatile("st.shared.u8 [%0], %1;" ::"r"(ubuf + (ub & ~15u) + lane), "r"(rem) : "memory");
+                        for (uint32_t o = ((ub + 15u) & ~15u) + 16u * lane; o < 992u * sl + 16u; o += 512u)
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ubuf + o), "r"(0u) : "memory");
+                    }
+                    if (k + 1 < n_full) load_unit(k + 1);
                     if (k == 0) {
                         // the 4 bytes before the unit and the bytes before the list: zeros
                         if (static_cast<uint32_t>(lane) < 4u + stray)
                             asm volatile("st.shared.u8 [%0], %1;" ::"r"(ubuf - 4u + lane), "r"(0u) : "memory");
-                        __syncwarp();
                     }
+                    __syncwarp();
                     // the dp2a path's carry counts every byte before the slice
                     uint32_t wb = 0;
                     if (k > 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
                     uint32_t cb = carry + tail_value(wb);
                     uint32_t* op = L.out + run - (k == 0 ? stray : 0u);
                     const uint32_t* const lim = L.out + limit;
-                    const int sl = n_sl - 4 * k < 4 ? n_sl - 4 * k : 4;  // this unit's slices
+                    const long long u_lo = U0 + static_cast<long long>(k) * kLUnit;
                     int i = 0;
 #pragma unroll 1
-                    for (; i < sl; ++i)
+                    for (; i < sl; ++i) {
+                        uint32_t end_off = 0;
+                        const uint32_t pad = 992u * (i + 1) > ub ? 992u * (i + 1) - ub : 0u;  // (the unit's last slice)
                         if (!slice_d3_odd<8, true>(ubuf, 992u * i, st_base, op, cb, lane, pol,
-                                                   (k == 0 && i == 0) ? stray : 0u, lim))
+                                                   (k == 0 && i == 0) ? stray : 0u, lim, &end_off, pad))
                             break;
-                    const long long u_lo = U0 + static_cast<long long>(k) * kLUnit;
+                        if (end_off) {  // integer count-1 ended the slice: the list is done
+                            if (lane == 0) s_count_end[wid] = u_lo + 992 * i + end_off - R.lo;
+                            ++i;
+                            break;
+                        }
+                    }
                     const uint32_t done = 992u * i;  // unit bytes decoded by slices
                     if (done > 0) {
                         // back to the general convention at u_lo + done
@@ -173,12 +208,13 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(we) : "r"(ubuf + done - 4u) : "memory");
                         carry = cb - tail_value(we);
                     }
-                    qs = u_lo + done;
-                    if (i < sl) {
+                    qs = u_lo + done < R.hi ? u_lo + done : R.hi;
+                    if (i < sl && run < limit) {
                         // the rest of the unit through the general path (this unit's
                         // buffer is free: it reads global memory, its ring goes here)
-                        general(qs, u_lo + 992 * sl, buf0 + b * kUnitBuf);
-                        qs = u_lo + 992 * sl;
+                        const long long u_hi = u_lo + 992 * sl < R.hi ? u_lo + 992 * sl : R.hi;
+                        general(qs, u_hi, buf0 + b * kUnitBuf);
+                        qs = u_hi;
                     }
                 }
                 // (a count limit reached with the next unit's load in flight: let it land)
