@@ -858,7 +858,7 @@ def run_lists(args):
                          "frac_of_nominal_8000": achieved / NOMINAL_HBM_GBS, "frac": achieved / peak,
                          "traffic": load_ncu_traffic(w.name), "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
                          "kernel_ms_avg": statistics.mean(kern_ms), "kernel_ms_min": min(kern_ms),
-                         "kernel": "vbyte_lists_decode (one launch per batch; rank 0's list range)"},
+                         "kernel": "vbyte_lists_decode_units (one launch per batch; rank 0's list range)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": n_bytes + 2 * (n_lists + 1) * 8,
