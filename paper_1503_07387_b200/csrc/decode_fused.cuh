@@ -53,6 +53,9 @@ namespace mvbk {
 #ifndef MVB_F_PF
 #define MVB_F_PF 8  // L2 prefetch distance of the unit loads, in eighths of a round of tickets (0: none)
 #endif
+#ifndef MVB_F_PF0
+#define MVB_F_PF0 1  // rounds of units prefetched into L2 before the wait for the previous grid
+#endif
 #ifndef MVB_F_LATE
 #define MVB_F_LATE 0  // 1: a unit's prefix entries are checked (and waited for) after the next unit's publication
 #endif
@@ -1048,6 +1051,30 @@ __device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uin
                  : "memory");
 }
 
+// Timeline build (-DMVB_F_TRACE=1, scripts/r2/trace_fused.py): every warp
+// appends (globaltimer, code) pairs to its 64-entry row of g_ftrace.
+#ifndef MVB_F_TRACE
+#define MVB_F_TRACE 0
+#endif
+#if MVB_F_TRACE
+__device__ unsigned long long* g_ftrace;
+#define MVB_FT(code)                                                                                    \
+    do {                                                                                                \
+        if (lane == 0 && g_ftrace) {                                                                    \
+            unsigned long long* row = g_ftrace + 64ull * (blockIdx.x * kSegWarps + wid);                \
+            unsigned long long t_;                                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+            const unsigned long long n_ = row[0];                                                       \
+            if (n_ < 62) {                                                                              \
+                row[1 + n_] = (t_ << 4) | (code);                                                       \
+                row[0] = n_ + 1;                                                                        \
+            }                                                                                           \
+        }                                                                                               \
+    } while (0)
+#else
+#define MVB_FT(code) ((void)0)
+#endif
+
 // kMode: 0 totals and decode, 1 totals only, 2 decode only (F.mode == kMode;
 // separate instantiations keep the common one free of the others' code)
 template <bool kDelta, int kMode>
@@ -1067,15 +1094,33 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     }
     __syncwarp();
     uint32_t phases = 0;  // bit b: parity of buffer b's next completion
+    MVB_FT(1);
     const ByteRange R = {S.in - S.mis, S.mis, S.mis + S.len, S.mis, S.mis + S.len};
     const long long q_stream_end = (R.hi + 15) & ~15ll;
     const RangeSink K = {S.hdr, nullptr, nullptr, nullptr};
     const unsigned long long pol = l2_evict_first();  // (output copies: written once, never read here)
+#if MVB_F_PF0
+    // While the previous grid on the stream drains: L2 prefetches of the units
+    // the first MVB_F_PF0 rounds of tickets will hand out (whichever warps take
+    // them).  Only prefetches may come before the wait -- L2 stays coherent with
+    // whatever still writes the input; a load into shared memory could be stale.
+    if (kMode != 1 && lane == 0) {
+        const long long w_all = static_cast<long long>(gridDim.x) * kSegWarps;
+#pragma unroll
+        for (int r = 0; r < MVB_F_PF0; ++r) {
+            const long long q = ((blockIdx.x * kSegWarps + wid) + r * w_all) * kUnit;
+            if (q - 16 >= R.lo && q + kUnit <= R.hi)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(R.ab + q), "r"(static_cast<uint32_t>(kUnit))
+                             : "memory");
+        }
+    }
+#endif
     // the previous grid on the stream (e.g. the previous decode on this
     // workspace: it resets the ticket and advances the epoch) is complete and
     // visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    MVB_FT(2);
     // this launch's tree tag; a decode-only launch reads the tree its totals
     // launch (the previous one on this workspace) tagged
     const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(&S.hdr->epoch);
@@ -1084,9 +1129,19 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     // units [u_first, u_end) are staged in shared memory by the TMA: the unit and
     // the 16 bytes before it lie inside the stream
-    const uint32_t u_first = static_cast<uint32_t>((R.lo + 16 + kUnit - 1) / kUnit);
+    // (unit 0 of a 16-byte-aligned stream is staged too: nothing lies before it, its
+    // 16 bytes before are zeroed in shared memory -- the stream's start is an
+    // integer boundary)
     const uint32_t u_end = static_cast<uint32_t>(R.hi / kUnit);
+    const uint32_t u_first = R.lo == 0 ? 0u : static_cast<uint32_t>((R.lo + 16 + kUnit - 1) / kUnit);
     const uint32_t n_units = static_cast<uint32_t>(S.n_seg);
+    // the stream's last, partial unit is staged as well (whole 16-byte blocks by the
+    // TMA, the last bytes one per lane, zeros after them): its totals pass and the
+    // whole slices of its decode read shared memory like any other unit's.  Left
+    // to masked global loads it was the decode's tail: 7.7 + 15.5 us of one warp
+    // on c2, a third of the launch.
+    const uint32_t part_bytes = static_cast<uint32_t>(R.hi - static_cast<long long>(u_end) * kUnit);
+    const uint32_t u_part = (part_bytes != 0u && u_end >= 1u) ? u_end : 0xFFFFFFFFu;
     unsigned* const ticket = reinterpret_cast<unsigned*>(&S.hdr->ticket);  // (units < 2^28: the low word)
 #if MVB_F_PF
     const uint32_t pf_dist = MVB_F_PF * gridDim.x * kSegWarps / 8u;
@@ -1101,7 +1156,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
             const long long qs = static_cast<long long>(up) * kUnit;
             const long long qe = qs + kUnit < q_stream_end ? qs + kUnit : q_stream_end;
-            const bool staged = up >= u_first && up < u_end;  // (warp-uniform)
+            const bool staged = (up >= u_first && up < u_end) || up == u_part;  // (warp-uniform)
             const uint32_t ubuf = staged ? buf0 + bp * kUnitBuf + 16u : 0u;
             if (unit_is_d3(up, base, c_up, f_up)) {
                 // (carry: every byte before the unit)
@@ -1128,16 +1183,45 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             }
         }
     };
-    auto load_unit = [&](uint32_t u, int b) -> bool {  // TMA of unit u into buffer b (if inside the stream)
-        const bool st = u >= u_first && u < u_end;  // (warp-uniform)
-        if (st && lane == 0)
-            tma_bulk_load(buf0 + b * kUnitBuf, R.ab + static_cast<long long>(u) * kUnit - 16, kUnit + 16, bar0 + 8u * b);
+    auto load_unit = [&](uint32_t u, int b) -> bool {  // TMA of unit u into buffer b (if it is staged)
+        const bool full = u >= u_first && u < u_end;
+        const bool st = full || u == u_part;  // (warp-uniform)
+        if (st && lane == 0) {
+            const uint8_t* const src = R.ab + static_cast<long long>(u) * kUnit;
+            const uint32_t bytes = full ? static_cast<uint32_t>(kUnit) : part_bytes & ~15u;
+            if (u == 0) tma_bulk_load(buf0 + b * kUnitBuf + 16u, src, bytes, bar0 + 8u * b);
+            else tma_bulk_load(buf0 + b * kUnitBuf, src - 16, bytes + 16u, bar0 + 8u * b);
+        }
         return st;
     };
-    auto wait_unit = [&](int b) {
+    // wait for unit u's bytes in buffer b; the edge units' shared-memory fix-ups
+    auto wait_unit = [&](uint32_t u, int b) {
         while (!mbar_test(bar0 + 8u * b, (phases >> b) & 1u)) {
         }
         phases ^= 1u << b;
+        if (u == 0 || u == u_part) {
+            const uint32_t ub = buf0 + b * kUnitBuf;
+            if (u == 0 && lane < 4) asm volatile("st.shared.u32 [%0], %1;" ::"r"(ub + 4u * lane), "r"(0u) : "memory");
+            if (u == u_part) {
+                const uint32_t tb = part_bytes & ~15u;
+                if (lane < 16) {
+                    const uint32_t v = static_cast<uint32_t>(lane) < part_bytes - tb
+                                           ? R.ab[static_cast<long long>(u) * kUnit + tb + lane]
+                                           : 0u;
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(ub + 16u + tb + lane), "r"(v) : "memory");
+                }
+                for (uint32_t o = tb + 16u + 16u * lane; o < static_cast<uint32_t>(kUnit); o += 512u)
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ub + 16u + o), "r"(0u) : "memory");
+            }
+            __syncwarp();
+        }
+    };
+    // totals of the staged unit u in buffer b (the zeros after a partial unit's
+    // bytes count as integers -- the first may close one the stream leaves
+    // unfinished -- and add nothing to the sum)
+    auto staged_totals = [&](uint32_t u, int b, unsigned& c_u, uint32_t& su, uint32_t& f_u) {
+        unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+        if (u == u_part) c_u -= static_cast<unsigned>(kUnit) - part_bytes;
     };
     auto take_ticket = [&]() -> uint32_t {
         unsigned t = 0;
@@ -1165,8 +1249,8 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             unsigned c_u;
             uint32_t su, f_u;
             if (load_unit(u, 0)) {
-                wait_unit(0);
-                unit_totals<kDelta>(buf0 + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+                wait_unit(u, 0);
+                staged_totals(u, 0, c_u, su, f_u);
             } else {
                 const long long qs = static_cast<long long>(u) * kUnit;
                 fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
@@ -1194,7 +1278,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             const FEntry* e = F.tree[0] + u;
             fentry_get(e, tag, c_e, s_e);
             const uint32_t f_e = static_cast<uint32_t>((__ldcg(&e->s) >> 24) & 0xFFu);
-            if (st) wait_unit(b);
+            if (st) wait_unit(u, b);
             if (base < S.count) decode_unit(u, b, base, csum, static_cast<unsigned>(c_e), f_e);
             __syncwarp();  // (buffer b is refilled next iteration)
             u = un;
@@ -1222,6 +1306,16 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
         uint32_t f_up = 0;
         for (;;) {
             const uint32_t u = take_ticket();
+            MVB_FT(3);
+#if MVB_F_TRACE
+            if (lane == 0 && g_ftrace) {  // (the unit taken, as a pseudo-event of code 9)
+                unsigned long long* row = g_ftrace + 64ull * (blockIdx.x * kSegWarps + wid);
+                if (row[0] < 62) {
+                    row[1 + row[0]] = (static_cast<unsigned long long>(u) << 4) | 9ull;
+                    row[0] += 1;
+                }
+            }
+#endif
             const int b = bp ^ 1;
             unsigned c_u = 0;
             uint32_t f_u = 0;
@@ -1234,22 +1328,26 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
             if (have_up) {
                 fused_prefix_issue(F, up, lane, P);
                 if (!MVB_F_LATE) fused_prefix_finish(F, up, tag, lane, P, base, csum);
+                MVB_FT(6);
             }
             if (u < n_units) {
                 uint32_t su;
                 if (u_staged) {
-                    wait_unit(b);
-                    unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+                    wait_unit(u, b);
+                    MVB_FT(4);
+                    staged_totals(u, b, c_u, su, f_u);
                 } else {
                     const long long qs = static_cast<long long>(u) * kUnit;
                     fused_totals<kDelta>(S, qs, qs + kUnit, lane, c_u, su, 0u, &f_u);
                 }
                 fused_publish(F, 0, u, c_u, su, tag, lane, f_u);
+                MVB_FT(5);
             }
             if (have_up) {
                 if (MVB_F_LATE) fused_prefix_finish(F, up, tag, lane, P, base, csum);
                 decode_unit(up, bp, base, csum, c_up, f_up);
                 __syncwarp();  // (buffer bp is refilled next iteration)
+                MVB_FT(7);
             }
             if (u >= n_units) break;
             have_up = true;
@@ -1261,6 +1359,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
 #if MVB_BULK_OUT
         stage_wait_all(lane);
 #endif
+        MVB_FT(8);
     }
     fused_complete(F, tag);
 }

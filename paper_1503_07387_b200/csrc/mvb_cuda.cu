@@ -1152,6 +1152,12 @@ int mvb_encode_deltas(const uint32_t* sorted_values, size_t n, uint8_t* out, siz
 
 // Internal profiling switch (not part of include/mvb_cuda.h), see g_kernel_choice.
 void mvbx_set_kernel(int choice) { g_kernel_choice = choice; }
+#if MVB_F_TRACE
+// (timeline build) rows of 64 u64 per warp of the fused decoder's grid, zeroed by the caller
+int mvbx_set_fused_trace(unsigned long long* dev_rows) {
+    return cudaMemcpyToSymbol(mvbk::g_ftrace, &dev_rows, sizeof(dev_rows)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // Internal profiling entry (not part of include/mvb_cuda.h): the calling
 // thread's last pipelined host decode as t[4k + {0,1,2,3}] = ms from its start
