@@ -73,12 +73,40 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
     uint32_t phases = 0;  // bit b: parity of buffer b's next completion
     const unsigned long long pol = l2_evict_first();
     unsigned* const ticket = reinterpret_cast<unsigned*>(&L.hdr->ticket);
+    // One list of lookahead in lane 0, spread over the current list's slices so
+    // that no step waits for the one before: the next ticket (taken when this
+    // list starts), its list index (order[]), that list's first byte offset,
+    // and an L2 prefetch of its first unit.  (Per list, the chain ticket ->
+    // order -> offsets -> first bytes is four memory latencies; a warp decodes
+    // ~28 lists of config 3.)
+    const unsigned n_lists32 = static_cast<unsigned>(L.n_lists);
+    unsigned t_nx = 0, l_nx = 0;
+    unsigned long long b0_nx = 0;
+    int la = 0;  // (warp-uniform) lookahead steps done for t_nx: 0 ticket taken, 1 list index loaded, 2 offset loaded, 3 prefetched
+    if (lane == 0) t_nx = atomicAdd(ticket, 1u);
+    auto lookahead = [&]() {  // one more step for the next list (the loads: lane 0)
+        if (la >= 3) return;
+        if (lane == 0 && t_nx < n_lists32) {
+            if (la == 0) l_nx = L.order ? L.order[t_nx] : t_nx;
+            else if (la == 1) b0_nx = L.byte_off[l_nx];
+            else {
+                const long long q = (L.mis0 + static_cast<long long>(b0_nx)) & ~15ll;
+                const long long left = ((L.mis0 + L.in_len) & ~15ll) - q;
+                if (left >= 16)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(L.ab + q),
+                                 "r"(static_cast<uint32_t>(left < kLUnit ? left : kLUnit))
+                                 : "memory");
+            }
+        }
+        ++la;
+    };
     while (true) {
-        unsigned t = 0;
-        if (lane == 0) t = atomicAdd(ticket, 1u);
-        const long long k_list = __shfl_sync(0xFFFFFFFFu, t, 0);
-        if (k_list >= L.n_lists) break;
-        const long long l = L.order ? static_cast<long long>(L.order[k_list]) : k_list;
+        while (la < 2) lookahead();  // (a short previous list: finish the chain up to the list index and offset)
+        const unsigned k_list = __shfl_sync(0xFFFFFFFFu, t_nx, 0);
+        if (k_list >= n_lists32) break;
+        const long long l = __shfl_sync(0xFFFFFFFFu, l_nx, 0);
+        if (lane == 0) t_nx = atomicAdd(ticket, 1u);
+        la = 0;
         long long b0 = static_cast<long long>(L.byte_off[l]), b1 = static_cast<long long>(L.byte_off[l + 1]);
         if (b1 > L.in_len) b1 = L.in_len;  // never read past in + in_len
         if (b0 > b1) b0 = b1;
@@ -189,6 +217,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
                     int i = 0;
 #pragma unroll 1
                     for (; i < sl; ++i) {
+                        lookahead();
                         uint32_t end_off = 0;
                         const uint32_t pad = 992u * (i + 1) > ub ? 992u * (i + 1) - ub : 0u;  // (the unit's last slice)
                         if (!slice_d3_odd<8, true>(ubuf, 992u * i, st_base, op, cb, lane, pol,
