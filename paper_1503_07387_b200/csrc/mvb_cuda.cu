@@ -19,6 +19,8 @@
 #include "../../include/mvb_cuda.h"
 #include "decode_kernel.cuh"
 #include "decode_seg.cuh"
+#include <nvtx3/nvToolsExt.h>
+
 #include "decode_fused.cuh"
 #include "decode_lists.cuh"
 #include "totals_kernel.cuh"
@@ -29,6 +31,14 @@
 #endif
 
 namespace {
+// NVTX range for timeline tools; balanced on every return path.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 using mvbk::Params;
 using mvbk::WsHeader;
@@ -582,6 +592,7 @@ bool g_pipe_grow = true;          // (tests: false keeps every chunk at g_pipe_c
 template <bool Delta>
 int decode_host_pipelined(HostCtx& c, const uint8_t* in, size_t scan, size_t count, uint32_t prev, uint32_t* out,
                           mvb_result* res) {
+    const NvtxRange range("mvb_decode_stream.pipelined");
     Params p = {};
     p.in = c.d_in;
     p.mis = 0;  // cudaMalloc'd: aligned
@@ -824,6 +835,7 @@ template <bool Delta>
 int lists_host(const uint8_t* in, size_t in_len, const unsigned long long* byte_off,
                const unsigned long long* int_off, const uint32_t* prev, size_t n_lists, uint32_t* out, int mode,
                mvb_result* results) {
+    const NvtxRange range("mvb_decode_lists.pipelined");
     if (n_lists == 0) return 0;
     if (byte_off == nullptr || int_off == nullptr || (in == nullptr && in_len > 0)) return MVB_ERR_INVALID_ARG;
     if (mode != MVB_STRICT) return MVB_ERR_INVALID_ARG;
@@ -1048,6 +1060,8 @@ int mvb_decode_delta_sharded(int n, const int* devices, const uint8_t* const* sh
         const int rc = shard_ctx(g, devices[g], shard_len[g], C[g]);
         if (rc) return rc;
     }
+    const NvtxRange whole("mvb_decode_delta_sharded");
+    nvtxMarkA("mvb.sharded.totals");
     // 1. totals of every shard but the last (one read of its bytes each), on
     //    each shard's own stream and device, concurrently
     std::vector<unsigned long long> rec(2 * n, 0);
@@ -1058,10 +1072,12 @@ int mvb_decode_delta_sharded(int n, const int* devices, const uint8_t* const* sh
         if (cudaMemcpyAsync(&rec[2 * g], C[g]->rec, 16, cudaMemcpyDeviceToHost, C[g]->stream) != cudaSuccess)
             return MVB_ERR_CUDA;
     }
+    nvtxMarkA("mvb.sharded.exchange");
     // 2. the exchange: 16 bytes per shard, through the host
     for (int g = 0; g + 1 < n; ++g)
         if (cudaSetDevice(devices[g]) != cudaSuccess || cudaStreamSynchronize(C[g]->stream) != cudaSuccess)
             return MVB_ERR_CUDA;
+    nvtxMarkA("mvb.sharded.decode");
     // 3. every shard decodes its part of the first `count` integers from its carry
     std::vector<unsigned long long> off(n, 0), want(n, 0), byte0(n, 0);
     uint32_t carry = prev;
@@ -1084,6 +1100,7 @@ int mvb_decode_delta_sharded(int n, const int* devices, const uint8_t* const* sh
                                MVB_STRICT, C[g]->res, C[g]->ws, C[g]->ws_cap, C[g]->stream);
         if (rc) return rc;
     }
+    nvtxMarkA("mvb.sharded.result");
     // 4. the whole-stream DecodeResult: the first shard that is not OK decides
     std::vector<mvb_result> r(n);
     for (int g = 0; g < n; ++g) {

@@ -363,11 +363,19 @@ class DeviceShard:
             raise RuntimeError(f"shard decode failed ({rc})")
 
     def run(self):
-        """One pass over the shard (queued on the current stream)."""
+        """One pass over the shard (queued on the current stream).  NVTX ranges
+         mark the three phases for timeline tools."""
+        nvtx = self.torch.cuda.nvtx
+        nvtx.range_push("mvb.shard.totals")
         self.prepass()
+        nvtx.range_pop()
         if self.delta and self.world > 1:
+            nvtx.range_push("mvb.shard.exchange")
             self.exchange()
+            nvtx.range_pop()
+        nvtx.range_push("mvb.shard.decode")
         self.decode()
+        nvtx.range_pop()
 
     def local_result(self) -> List[int]:
         """(status, written, consumed, start, requested) with a clean end read as OK."""
