@@ -363,6 +363,19 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // streams of few units per warp: the instantiation whose first round of units
+    // is handed out without tickets (same registers and shared memory: the grid
+    // above fits it)
+    if (Mode == 0 && MVB_F_STATIC0 > 0 && f.n_seg < MVB_F_STATIC0 * f.W) {
+        int sms2 = 0;
+        const int per_sm2 = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, true>),
+                                      mvbk::kSegThreads, mvbk::kFSmem, &sms2);
+        if (per_sm2 >= per_sm) {
+            if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, true>, F) != cudaSuccess)
+                return MVB_ERR_CUDA;
+            return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+        }
+    }
     if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode>, F) != cudaSuccess) return MVB_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
 }
