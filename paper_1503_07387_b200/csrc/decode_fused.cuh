@@ -580,6 +580,21 @@ __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, uint32_t* op, uint
     (void)slice_d3_odd<9>(ubuf, 2976u, st_base, op, carry, lane, pol);
 }
 
+// A staged delta unit with integers of 4 or 5 bytes (its integers all end
+// before lim): checked slices, a second dp2a chain where the long integers
+// are.  False if a slice holds a malformed integer (the caller then decodes
+// the unit again with the general path, which reports it; the slices stored so
+// far are what it stores).
+__device__ __noinline__ bool unit_d3_checked(uint32_t ubuf, uint32_t* op, uint32_t carry, uint32_t st_base,
+                                             const uint32_t* lim, unsigned long long pol) {
+    const int lane = threadIdx.x & 31;
+    uint32_t eo;
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i)
+        if (!slice_d3_odd<8, true>(ubuf, 992u * i, st_base, op, carry, lane, pol, 0u, lim, &eo)) return false;
+    return slice_d3_odd<9, true>(ubuf, 2976u, st_base, op, carry, lane, pol, 0u, lim, &eo);
+}
+
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
 // shared memory at ubuf (byte qs; the 16 bytes before it too), or -- ubuf 0,
 // units at the stream's edges -- read from global memory with range masks.
@@ -1083,7 +1098,11 @@ __device__ unsigned long long* g_ftrace;
 // kStatic0 (mode 0, streams of few units per warp): the first round of units
 // is handed out without tickets (a separate instantiation: the long streams'
 // kernel stays as it is).
-template <bool kDelta, int kMode, bool kStatic0 = false>
+// kLong (delta streams of 2.5+ bytes per integer): units with integers of 4
+// or 5 bytes take checked dp2a slices instead of the general path (a separate
+// instantiation as well: hooked into the common kernel, the extra call cost
+// c4 4%).
+template <bool kDelta, int kMode, bool kStatic0 = false, bool kLong = false>
 __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(const __grid_constant__ FusedParams F) {
     extern __shared__ __align__(128) uint8_t smem[];
     const SegParams& S = F.S;
@@ -1169,6 +1188,9 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 uint32_t carry = csum + prev0;
                 uint32_t* op = S.out + base;
                 decode_unit_d3(ubuf, op, carry, st_base, lane, pol);
+            } else if (kLong && kDelta && up >= u_first && up < u_end && base + c_up < S.count &&
+                       unit_d3_checked(ubuf, S.out + base, csum + prev0, st_base, S.out + S.count, pol)) {
+                // (kLong: a unit with integers of 4 or 5 bytes took the checked slices)
             } else {
                 const bool swz = F.swz == 1 || (F.swz == 2 && range_dense(c_up, qe - qs));
                 uint32_t straddle = 0;
