@@ -46,3 +46,8 @@ for back_to_back in (0, 1):
     order = sorted(range(len(ev)), key=lambda i: -max(t for t, c in ev[i] if c != 9))[:4]
     for i in order:
         print("  slow warp:", " ".join((f"u={t}" if c == 9 else f"{c}@{(t - t0) / 1e3:.1f}") for t, c in ev[i]))
+    # the warps whose first publication is the latest (every later unit's prefix waits for them)
+    def first_pub(e):
+        return next((t for t, c in e if c == 5), 0)
+    for i in sorted(range(len(ev)), key=lambda i: -first_pub(ev[i]))[:6]:
+        print(f"  late first publication (warp row {i}):", " ".join((f"u={t}" if c == 9 else f"{c}@{(t - t0) / 1e3:.1f}") for t, c in ev[i][:8]))
