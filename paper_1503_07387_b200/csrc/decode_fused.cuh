@@ -377,6 +377,8 @@ __device__ __forceinline__ void slot_store_w(uint32_t& sp, uint32_t w, uint32_t 
 __device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t first, uint32_t end, uint32_t* ob, int lane,
                                              unsigned long long pol) {
     const uint32_t i0 = (first + 3u) & ~3u, i1 = end & ~3u;
+    // (the copied range lies in the staging buffer; the bulk copy's ends are 16-byte aligned)
+    MVB_CHECK(first <= end && end <= static_cast<uint32_t>(kFStage) && (reinterpret_cast<uintptr_t>(ob) & 15u) == 0u);
     if (lane < 8) {
         const uint32_t i = lane < 4 ? (first & ~3u) + static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
         if (lane < 4 ? (i >= first && i < i0 && i < end) : (i < end && i >= i0)) {

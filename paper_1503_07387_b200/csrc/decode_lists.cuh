@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
                     const uint8_t* src = R.ab + U0 + static_cast<long long>(k) * kLUnit;
                     const bool tma = k > 0 || tb > 0;  // (warp-uniform; units after the first always load their 16 bytes before)
                     tma_mask = (tma_mask & ~(1u << b)) | (tma ? 1u << b : 0u);
+                    // (everything loaded lies inside the caller's buffer and the unit buffer)
+                    MVB_CHECK(src >= R.ab + R.elo && src + ub <= R.ab + R.ehi && ub <= static_cast<uint32_t>(kLUnit) &&
+                              (k == 0 || src - 16 >= R.ab + R.elo));
                     if (tma && lane == 0) {
                         if (k == 0) tma_bulk_load(buf0 + 16u, src, tb, bar0);
                         else tma_bulk_load(buf0 + b * kUnitBuf, src - 16, tb + 16u, bar0 + 8u * b);
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_lists_decode_unit
                             break;
                         }
                     }
+                    MVB_CHECK(op <= lim);  // (the slices stored nothing at or past integer count)
                     const uint32_t done = 992u * i;  // unit bytes decoded by slices
                     if (done > 0) {
                         // back to the general convention at u_lo + done
