@@ -582,6 +582,111 @@ __device__ __forceinline__ void decode_unit_d3(uint32_t ubuf, uint32_t* op, uint
     (void)slice_d3_odd<9>(ubuf, 2976u, st_base, op, carry, lane, pol);
 }
 
+// A staged unit whose integers all have the same length L = 4 or 5 (sparse
+// streams: hashed ids, the all-5-byte point of BASELINE config 5 -- the
+// reference has a window kernel for just this shape, two5b_lanes,
+// decode_simd.cpp:68-79).  The terminators of such a unit form an arithmetic
+// progression, so integer j ends at byte e0 + L * j: instead of 32 byte slots
+// per lane (6 of them used), lane l assembles integers l, l + 32, ... -- two
+// ld.shared, a funnel shift, two dp4a -- and stores them straight to global
+// memory, consecutive lanes to consecutive integers (no staging).  Delta: one
+// warp scan per pass of 32 integers.
+//   ubuf: the unit in shared memory (the 16 bytes before it too); n_ints: its
+//   integers (the totals pass's count), all before the count limit; op: their
+//   place in the output; carry (delta): the value before the unit's first
+//   integer (complete integers only).
+// False -- nothing decided, the caller takes another path -- if the unit is not
+// of this shape, or (strict mode, internal.hpp:35) a fifth byte is >= 0x10;
+// what was stored until then is what the general path stores again.
+template <bool kDelta>
+__device__ __noinline__ bool unit_uniform(uint32_t ubuf, uint32_t n_ints, uint32_t* op, uint32_t carry) {
+    const int lane = threadIdx.x & 31;
+    // the first two terminators of the unit (in lane 0's 32 bytes): e0 and L
+    uint32_t T[kUnit / kLLSlice];
+#pragma unroll
+    for (int i = 0; i < kUnit / kLLSlice; ++i) {
+        const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * i + 32 * lane);
+        const uint4 x0 = lds128(sa), x1 = lds128(sa + 16u);
+        T[i] = hibits16(~x0.x, ~x0.y, ~x0.z, ~x0.w) | (hibits16(~x1.x, ~x1.y, ~x1.z, ~x1.w) << 16);
+    }
+    const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, T[0], 0);
+    const uint32_t t1 = t0 & (t0 - 1u);
+    if (t1 == 0u) return false;
+    const uint32_t e0 = __ffs(t0) - 1u, L = (__ffs(t1) - 1u) - e0;
+    if (L < 4u || L > 5u || e0 >= L) return false;
+    // the integer ending at e0 has L bytes too: a terminator (or the stream's start,
+    // zeros) at e0 - L, continuation bytes after it
+    bool ok = true;
+    if (lane < 5) {
+        const int pos = static_cast<int>(e0) - static_cast<int>(L) + lane;  // e0 - L .. e0 - L + 4
+        if (pos < 0) {
+            uint32_t b;
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(ubuf + pos) : "memory");
+            ok = lane == 0 ? b < 0x80u : b >= 0x80u;
+        }
+    }
+    // every lane's terminators are the progression's: bits r + k L of each 32-byte word
+    const uint32_t pat = L == 5u ? 0x42108421u : 0x11111111u;
+    uint32_t r = (e0 + L * 1024u - 32u * static_cast<uint32_t>(lane)) % L;  // first expected position in slice 0's lane bytes
+    const uint32_t step = L - (static_cast<uint32_t>(kLLSlice) % L);        // the same for the next slice: + step (mod L)
+#pragma unroll
+    for (int i = 0; i < kUnit / kLLSlice; ++i) {
+        ok = ok && T[i] == (pat << r);
+        r += step;
+        if (r >= L) r -= L;
+    }
+    const uint32_t n = (static_cast<uint32_t>(kUnit) - 1u - e0) / L + 1u;
+    if (!__all_sync(0xFFFFFFFFu, ok) || n != n_ints) return false;
+    // the gather: four passes of 32 integers per iteration, independent of one
+    // another (their shared-memory loads and, delta, their warp scans overlap)
+    constexpr int kQ = 4;
+    uint32_t bad = 0;
+    const uint32_t sh = 28u - 7u * L;  // (L = 4: 0)
+#pragma unroll 1
+    for (uint32_t j0 = 0; j0 < n; j0 += 32u * kQ) {
+        uint32_t v[kQ];
+        bool act[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const uint32_t j = j0 + 32u * q + static_cast<uint32_t>(lane);
+            act[q] = j < n;
+            const uint32_t a = ubuf + e0 + L * (act[q] ? j : 0u);  // the integer's last byte
+            uint32_t lo, hi;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"((a & ~3u) - 4u) : "memory");
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(a & ~3u) : "memory");
+            const uint32_t t = a & 3u;
+            const uint32_t x = __funnelshift_rc(lo, hi, 8u * t + 8u);  // bytes a - 3 .. a (t = 3: hi itself)
+            uint32_t w = pack28(x);
+            if (L == 5u) {
+                w = (w << 7) | ((lo >> (8u * t)) & 0x7Fu);  // the first byte: byte t of lo
+                bad |= act[q] ? (x >> 28) & 7u : 0u;        // the fifth byte's bits 4..6 (bit 7: a terminator)
+            } else {
+                w >>= sh;
+            }
+            v[q] = (act[q] || !kDelta) ? w : 0u;
+        }
+        if (kDelta) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v[q], o);
+                    if (lane >= o) v[q] += y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                v[q] += carry;
+                carry = __shfl_sync(0xFFFFFFFFu, v[q], 31);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            if (act[q]) __stcs(op + j0 + 32u * q + lane, v[q]);
+    }
+    return !__any_sync(0xFFFFFFFFu, bad != 0u);
+}
+
 // A staged delta unit with integers of 4 or 5 bytes (its integers all end
 // before lim): checked slices, a second dp2a chain where the long integers
 // are.  False if a slice holds a malformed integer (the caller then decodes
@@ -1100,10 +1205,11 @@ __device__ unsigned long long* g_ftrace;
 // kStatic0 (mode 0, streams of few units per warp): the first round of units
 // is handed out without tickets (a separate instantiation: the long streams'
 // kernel stays as it is).
-// kLong (delta streams of 2.5+ bytes per integer): units with integers of 4
-// or 5 bytes take checked dp2a slices instead of the general path (a separate
-// instantiation as well: hooked into the common kernel, the extra call cost
-// c4 4%).
+// kLong (delta streams asked for at 2.5+ bytes per integer, plain ones at 4+):
+// units of equally long 4- or 5-byte integers take the per-integer gather
+// (unit_uniform), other delta units with integers of 4 or 5 bytes checked dp2a
+// slices, instead of the general path (a separate instantiation as well:
+// hooked into the common kernel, the extra call cost c4 4%).
 template <bool kDelta, int kMode, bool kStatic0 = false, bool kLong = false>
 __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(const __grid_constant__ FusedParams F) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1178,6 +1284,19 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     auto unit_is_d3 = [&](uint32_t up, unsigned long long base, unsigned c_up, uint32_t f_up) -> bool {
         return kDelta && up >= u_first && up < u_end && !(f_up & 1u) && base + c_up < S.count;
     };
+    // (kLong) unit_uniform with the general path's carry: the sum of the complete integers before the unit
+    auto unit_uniform_at = [&](uint32_t ubuf, unsigned c_up, uint32_t* op, uint32_t csum) -> bool {
+        uint32_t carry = 0;
+        if (kDelta) {
+            uint32_t wb;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wb) : "r"(ubuf - 4u) : "memory");
+            carry = csum - tail_value(wb) + prev0;
+        }
+#if MVB_BULK_OUT
+        stage_wait_read(lane);  // (no staging here, but a later general fallback rewrites the buffer)
+#endif
+        return unit_uniform<kDelta>(ubuf, c_up, op, carry);
+    };
     // decode unit `up` (buffer bp), given its prefix and its totals pass's count / flags
     auto decode_unit = [&](uint32_t up, int bp, unsigned long long base, uint32_t csum, unsigned c_up, uint32_t f_up) {
         if (base < S.count) {  // (warp-uniform; otherwise nothing of unit up is stored)
@@ -1190,6 +1309,9 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 uint32_t carry = csum + prev0;
                 uint32_t* op = S.out + base;
                 decode_unit_d3(ubuf, op, carry, st_base, lane, pol);
+            } else if (kLong && up >= u_first && up < u_end && base + c_up < S.count && 7u * c_up <= 2u * kUnit &&
+                       unit_uniform_at(ubuf, c_up, S.out + base, csum)) {
+                // (kLong: a unit of equally long 4- or 5-byte integers took the gather)
             } else if (kLong && kDelta && up >= u_first && up < u_end && base + c_up < S.count &&
                        unit_d3_checked(ubuf, S.out + base, csum + prev0, st_base, S.out + S.count, pol)) {
                 // (kLong: a unit with integers of 4 or 5 bytes took the checked slices)

@@ -363,16 +363,19 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // delta streams of long integers (2.5+ bytes per integer asked for): units with
-    // integers of 4 or 5 bytes take checked dp2a slices
-    if (Delta && Mode == 0 && 2 * p.len >= 5 * static_cast<long long>(p.count)) {
+    // streams of long integers (asked for at 2.5+ bytes per integer, delta; 4+,
+    // plain): the instantiation whose units of equally long 4-5-byte integers
+    // take the per-integer gather and whose other delta units with such integers
+    // take checked dp2a slices
+    if (Mode == 0 && (Delta ? 2 * p.len >= 5 * static_cast<long long>(p.count)
+                            : p.len >= 4 * static_cast<long long>(p.count))) {
         const bool st0 = MVB_F_STATIC0 > 0 && f.n_seg < MVB_F_STATIC0 * f.W;
-        const void* fn = st0 ? reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, true, Delta>)
-                             : reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, false, Delta>);
+        const void* fn = st0 ? reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, true, Mode == 0>)
+                             : reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, false, Mode == 0>);
         int sms2 = 0;
         if (occupancy(fn, mvbk::kSegThreads, mvbk::kFSmem, &sms2) >= per_sm) {
-            const cudaError_t e = st0 ? cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, true, Delta>, F)
-                                      : cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, false, Delta>, F);
+            const cudaError_t e = st0 ? cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, true, Mode == 0>, F)
+                                      : cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, false, Mode == 0>, F);
             if (e != cudaSuccess) return MVB_ERR_CUDA;
             return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
         }
