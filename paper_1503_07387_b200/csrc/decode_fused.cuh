@@ -955,7 +955,12 @@ __device__ __forceinline__ void fused_prefix(const FusedParams& F, long long v, 
 // fused_totals for a unit staged in shared memory (ubuf: its first byte; the
 // 16 bytes before it are there too): n_it 1 KiB iterations, all inside the
 // stream -- no range masks, 32-bit addressing.
-template <bool kDelta>
+// kLong (the long-integer instantiations): an iteration with integers of 4+
+// bytes adds the second chain's correction to the cheap weights -- a byte after
+// three (four) continuation bytes was counted as 2^14: (2^21 - 2^14) = 127 x
+// 2^14 and (2^28 - 2^14) = (127 + 16256) x 2^14 more, two dp4a over 0/1 class
+// flags -- instead of recomputing every weight exactly.
+template <bool kDelta, bool kLong = false>
 __device__ __forceinline__ void unit_totals(uint32_t ubuf, int n_it, int lane, unsigned& cnt_out, uint32_t& sum_out,
                                             uint32_t& flags_out) {
     uint32_t h1 = 0;  // lane 0: the word before the iteration
@@ -975,7 +980,22 @@ __device__ __forceinline__ void unit_totals(uint32_t ubuf, int n_it, int lane, u
             ftot_word(w[0], p1, cc, a, b, hi3);
 #pragma unroll
             for (int k = 1; k < 8; ++k) ftot_word(w[k], w[k - 1], cc, a, b, hi3);
-            if (__any_sync(0xFFFFFFFFu, hi3 != 0)) {  // an integer of 4+ bytes: the exact weights
+            if (kLong && __any_sync(0xFFFFFFFFu, hi3 != 0)) {
+                flags |= 1u;
+                uint32_t x3 = 0, x4 = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t ck = w[k] & 0x80808080u, cq = (k ? w[k - 1] : p1) & 0x80808080u;
+                    const uint32_t c3 = __funnelshift_l(cq, ck, 1) & __funnelshift_l(cq, ck, 9) & __funnelshift_l(cq, ck, 17);
+                    const uint32_t c4 = c3 & (cq >> 7);  // (byte j of the word before is byte j - 4)
+                    const uint32_t w7 = w[k] ^ ck;
+                    x3 = __dp4a(w7, c3, x3);
+                    x4 = __dp4a(w7, c4, x4);
+                }
+                sA += a;
+                sB += b;
+                sX += (127u * x3 + 16256u * x4) << 14;
+            } else if (__any_sync(0xFFFFFFFFu, hi3 != 0)) {  // an integer of 4+ bytes: the exact weights
                 flags |= 1u;
                 uint32_t p2 = __shfl_up_sync(0xFFFFFFFFu, w[6], 1);
                 if (lane == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(p2) : "r"(sa - 8u) : "memory");
@@ -1372,7 +1392,7 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
     // bytes count as integers -- the first may close one the stream leaves
     // unfinished -- and add nothing to the sum)
     auto staged_totals = [&](uint32_t u, int b, unsigned& c_u, uint32_t& su, uint32_t& f_u) {
-        unit_totals<kDelta>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
+        unit_totals<kDelta, kLong>(buf0 + b * kUnitBuf + 16u, kUnit / kLLSlice, lane, c_u, su, f_u);
         if (u == u_part) c_u -= static_cast<unsigned>(kUnit) - part_bytes;
     };
     // (kStatic0: the first round of units is handed out statically, unit = the warp's
