@@ -29,6 +29,7 @@ that invariance, decode_test.cpp:333-362).
 from __future__ import annotations
 
 import ctypes
+import weakref
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Union
@@ -212,7 +213,7 @@ class Decoder:
         self.res = torch.zeros(3, dtype=torch.int64, device=self.device)  # 24-byte mvb_result
         self.ws = None
         self.ws_bytes = 0
-        self._lists_ok = {}  # validated (offset tensors, versions) -> total integer count
+        self._lists_ok = []  # validated (offset tensors (weak), versions, total integer count), newest last
         self._ensure(capacity_bytes)
 
     def _ensure(self, in_len: int):
@@ -265,18 +266,23 @@ class Decoder:
                                         results.is_contiguous() and results.numel() >= 3 * n):
             raise MvbError("results must be a contiguous int64 CUDA tensor of >= 3 * n_lists entries")
         if n > 0:
-            # the offsets are validated once per tensor version (the check reads them
-            # back: a device synchronisation that repeated decodes of one batch skip)
-            key = (byte_offsets.data_ptr(), byte_offsets._version, int_offsets.data_ptr(), int_offsets._version, n)
-            total = self._lists_ok.get(key)
+            # the offsets are validated once per tensor object and version (the check
+            # reads them back: a device synchronisation that repeated decodes of one
+            # batch skip).  Identity, not address: a freed tensor's memory is reused.
+            total = None
+            for wb, wi, vb, vi, tot in self._lists_ok:
+                if wb() is byte_offsets and wi() is int_offsets and vb == byte_offsets._version and \
+                        vi == int_offsets._version:
+                    total = tot
+                    break
             if total is None:
                 io_h = int_offsets.cpu()
                 if bool((io_h[1:] < io_h[:-1]).any()) or bool((byte_offsets[1:] < byte_offsets[:-1]).any()):
                     raise MvbError("byte_offsets and int_offsets must be non-decreasing")
                 total = int(io_h[-1])
-                if len(self._lists_ok) >= 16:
-                    self._lists_ok.clear()
-                self._lists_ok[key] = total
+                self._lists_ok = [e for e in self._lists_ok if e[0]() is not None and e[1]() is not None][-7:]
+                self._lists_ok.append((weakref.ref(byte_offsets), weakref.ref(int_offsets), byte_offsets._version,
+                                       int_offsets._version, total))
             _check_out_tensor(out, total, inp.device)
         L = _lib.lib()
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731

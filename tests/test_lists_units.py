@@ -138,3 +138,31 @@ def test_three_byte_and_long_integers_across_unit_and_slice_seams(cuda, oracle):
                                     rng.integers(0, 1 << 7, 9000 - n_before, dtype=np.uint64)]).astype(np.uint32)
                 specs.append((oracle.encode_sequence(v), v.size, int(rng.integers(0, 1 << 32))))
     run_batch(cuda, oracle, specs, 3)
+
+
+def test_offset_validation_follows_tensor_identity_and_version(cuda, oracle):
+    """Decoder.decode_lists validates the offset tensors once per tensor object
+    and version: a new tensor at a reused address is validated again, and an
+    in-place change to decreasing offsets is caught."""
+    import torch
+
+    d = mvb.Decoder(cuda, 1 << 16)
+    rng = np.random.default_rng(3)
+    for n_each in (10, 500, 20):  # same number of lists, different totals; freed tensors' addresses get reused
+        vals = [gaps(rng, n_each) for _ in range(4)]
+        parts = [oracle.encode_sequence(v) for v in vals]
+        bo = np.zeros(5, np.int64)
+        bo[1:] = np.cumsum([p.size for p in parts])
+        io = np.zeros(5, np.int64)
+        io[1:] = np.cumsum([n_each] * 4)
+        src = torch.from_numpy(np.concatenate(parts)).to(cuda)
+        out = torch.zeros(4 * n_each, dtype=torch.int32, device=cuda)
+        d.decode_lists(src, torch.from_numpy(bo).to(cuda), torch.from_numpy(io).to(cuda), out, delta=True)
+        want = np.concatenate([np.cumsum(v, dtype=np.uint32) for v in vals])
+        np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), want)
+    t_bo, t_io = torch.from_numpy(bo).to(cuda), torch.from_numpy(io).to(cuda)
+    d.decode_lists(src, t_bo, t_io, out, delta=True)
+    d.decode_lists(src, t_bo, t_io, out, delta=True)  # (cached)
+    t_io[2] = 1  # decreasing now
+    with pytest.raises(mvb.MvbError):
+        d.decode_lists(src, t_bo, t_io, out, delta=True)
