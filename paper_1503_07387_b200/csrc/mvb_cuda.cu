@@ -367,30 +367,31 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
     // plain): the instantiation whose units of equally long 4-5-byte integers
     // take the per-integer gather and whose other delta units with such integers
     // take checked dp2a slices
-    if (Mode == 0 && (Delta ? 2 * p.len >= 5 * static_cast<long long>(p.count)
-                            : p.len >= 4 * static_cast<long long>(p.count))) {
+    if constexpr (Mode == 0) {
         const bool st0 = MVB_F_STATIC0 > 0 && f.n_seg < MVB_F_STATIC0 * f.W;
-        const void* fn = st0 ? reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, true, Mode == 0>)
-                             : reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, false, Mode == 0>);
-        int sms2 = 0;
-        if (occupancy(fn, mvbk::kSegThreads, mvbk::kFSmem, &sms2) >= per_sm) {
-            const cudaError_t e = st0 ? cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, true, Mode == 0>, F)
-                                      : cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, false, Mode == 0>, F);
-            if (e != cudaSuccess) return MVB_ERR_CUDA;
-            return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+        if (Delta ? 2 * p.len >= 5 * static_cast<long long>(p.count) : p.len >= 4 * static_cast<long long>(p.count)) {
+            const void* fn = st0 ? reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, 0, true, true>)
+                                 : reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, 0, false, true>);
+            int sms2 = 0;
+            if (occupancy(fn, mvbk::kSegThreads, mvbk::kFSmem, &sms2) >= per_sm) {
+                const cudaError_t e = st0 ? cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, 0, true, true>, F)
+                                          : cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, 0, false, true>, F);
+                if (e != cudaSuccess) return MVB_ERR_CUDA;
+                return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+            }
         }
-    }
-    // streams of few units per warp: the instantiation whose first round of units
-    // is handed out without tickets (same registers and shared memory: the grid
-    // above fits it)
-    if (Mode == 0 && MVB_F_STATIC0 > 0 && f.n_seg < MVB_F_STATIC0 * f.W) {
-        int sms2 = 0;
-        const int per_sm2 = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode, true>),
-                                      mvbk::kSegThreads, mvbk::kFSmem, &sms2);
-        if (per_sm2 >= per_sm) {
-            if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode, true>, F) != cudaSuccess)
-                return MVB_ERR_CUDA;
-            return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+        // streams of few units per warp: the instantiation whose first round of units
+        // is handed out without tickets (same registers and shared memory: the grid
+        // above fits it)
+        if (st0) {
+            int sms2 = 0;
+            const int per_sm2 = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, 0, true>),
+                                          mvbk::kSegThreads, mvbk::kFSmem, &sms2);
+            if (per_sm2 >= per_sm) {
+                if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, 0, true>, F) != cudaSuccess)
+                    return MVB_ERR_CUDA;
+                return cudaGetLastError() == cudaSuccess ? 0 : MVB_ERR_CUDA;
+            }
         }
     }
     if (cudaLaunchKernelEx(&cfg, mvbk::vbyte_fused_decode<Delta, Mode>, F) != cudaSuccess) return MVB_ERR_CUDA;
