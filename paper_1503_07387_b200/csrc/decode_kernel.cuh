@@ -135,6 +135,8 @@ struct Params {
     unsigned n_groups;
     mvb_result* res_dev;       // optional
     unsigned long long* trace; // optional per-tile timeline (profiling only): 8 x u64 per tile
+    int only_if_malformed;     // permissive decode after a strict pass of the same request: run only if that pass
+                               // reported a malformed integer (otherwise both modes decode alike and its result stands)
 };
 
 // Starting value of the delta scan: the host argument, plus the device-resident
@@ -578,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 5) vbyte_decode_kernel(Params P) {
     // a running CTA, so every tile waited on is resident whatever order the
     // hardware dispatches CTAs in (finalize_launch resets the ticket).
     __shared__ long long s_tile;
+    if (P.only_if_malformed && *reinterpret_cast<volatile int*>(&P.hdr->result.status) != MVB_MALFORMED) return;
     if (threadIdx.x == 0) s_tile = static_cast<long long>(atomicAdd(&P.hdr->ticket, 1ull));
     __syncthreads();
     const long long t = s_tile;

@@ -314,8 +314,11 @@ FusedPlan fused_plan(long long qlen, long long W_max) {
     return f;
 }
 
+// extra_bytes / extra_out: room after the tree for a second kernel's arrays (the
+// permissive decode's), part of the same workspace layout.
 template <bool Delta, int Mode>
-int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, unsigned long long* rec) {
+int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, unsigned long long* rec,
+                   size_t extra_bytes = 0, char** extra_out = nullptr) {
     constexpr int mode = Mode;
     int sms = 0;
     const int per_sm = occupancy(reinterpret_cast<const void*>(mvbk::vbyte_fused_decode<Delta, Mode>), mvbk::kSegThreads,
@@ -323,7 +326,8 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
     if (per_sm < 0) return MVB_ERR_CUDA;
     const long long W_max = static_cast<long long>(per_sm) * sms * mvbk::kSegWarps;
     const FusedPlan f = fused_plan(p.mis + p.len, W_max);
-    if (ws_bytes < f.need) return MVB_ERR_WORKSPACE;
+    if (ws_bytes < f.need + extra_bytes) return MVB_ERR_WORKSPACE;
+    if (extra_out) *extra_out = static_cast<char*>(ws) + f.need;
     mvbk::FusedParams F = {};
     mvbk::SegParams& S = F.S;
     S.in = p.in;
@@ -351,8 +355,8 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
         b += l ? 4 * static_cast<size_t>(f.n_at[l]) : 0;
         b = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(b) + 15) & ~static_cast<uintptr_t>(15));
     }
-    const unsigned long long layout = (6ull << 56) ^ static_cast<unsigned long long>(f.n_seg);
-    if (prepare_workspace(ws, f.need, layout, s) != cudaSuccess) return MVB_ERR_CUDA;
+    const unsigned long long layout = ((extra_bytes ? 7ull : 6ull) << 56) ^ static_cast<unsigned long long>(f.n_seg);
+    if (prepare_workspace(ws, f.need + extra_bytes, layout, s) != cudaSuccess) return MVB_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(f.W / mvbk::kSegWarps));
     cfg.blockDim = dim3(mvbk::kSegThreads);
@@ -400,10 +404,10 @@ int launch_fused_m(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, u
 
 template <bool Delta>
 int launch_fused(const Params& p, void* ws, size_t ws_bytes, cudaStream_t s, int mode = 0,
-                 unsigned long long* rec = nullptr) {
+                 unsigned long long* rec = nullptr, size_t extra_bytes = 0, char** extra_out = nullptr) {
     if (mode == 1) return launch_fused_m<true, 1>(p, ws, ws_bytes, s, rec);
     if (mode == 2) return launch_fused_m<true, 2>(p, ws, ws_bytes, s, rec);
-    return launch_fused_m<Delta, 0>(p, ws, ws_bytes, s, rec);
+    return launch_fused_m<Delta, 0>(p, ws, ws_bytes, s, rec, extra_bytes, extra_out);
 }
 
 int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, uint32_t prev,
@@ -444,6 +448,32 @@ int decode_device(const uint8_t* in, size_t in_len, size_t count, bool delta, ui
     if (mode == MVB_STRICT && g_kernel_choice == 6)
         return delta ? launch_seg<true>(p, ws, ws_bytes, stream) : launch_seg<false>(p, ws, ws_bytes, stream);
     // per-tile kernel: permissive mode (and strict choice 1)
+    p.only_if_malformed = 0;
+    char* arrays = static_cast<char*>(ws) + kHeaderBytes;
+    if (mode == MVB_PERMISSIVE && g_kernel_choice == 0) {
+        // A stream without a malformed integer decodes alike in both modes
+        // (internal.hpp:35-36 is the only difference): the strict single-read
+        // decoder runs first, and the permissive kernel -- three to five times
+        // slower -- only if that pass reported one (its CTAs check the result the
+        // strict pass left in the header and return otherwise).  The two kernels'
+        // arrays sit side by side in the workspace.
+        const size_t extra = ws_need(tiles) - kHeaderBytes;
+        const int rc = delta ? launch_fused<true>(p, ws, ws_bytes, stream, 0, nullptr, extra, &arrays)
+                             : launch_fused<false>(p, ws, ws_bytes, stream, 0, nullptr, extra, &arrays);
+        if (rc) return rc;
+        p.only_if_malformed = 1;
+        p.dcnt = reinterpret_cast<unsigned long long*>(arrays);
+        p.dsum = p.dcnt + tiles;
+        p.dmax = p.dsum + tiles;
+        p.n_groups = static_cast<unsigned>(groups_for(tiles));
+        p.gcnt = p.dmax + tiles;
+        p.gsum = p.gcnt + p.n_groups;
+        p.gacc_cnt = p.gsum + p.n_groups;
+        p.gacc_sum = p.gacc_cnt + p.n_groups;
+        const cudaError_t e = delta ? launch<true, mvbk::MODE_PERMISSIVE>(p, stream)
+                                    : launch<false, mvbk::MODE_PERMISSIVE>(p, stream);
+        return e == cudaSuccess ? 0 : MVB_ERR_CUDA;
+    }
     const size_t need = ws_need(tiles);
     if (ws_bytes < need) return MVB_ERR_WORKSPACE;
     p.dcnt = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + kHeaderBytes);
@@ -775,7 +805,8 @@ size_t mvb_workspace_bytes(size_t in_len) {
     // of 16-byte entries (+ 4-byte arrival counters above level 0)
     const size_t fs = (in_len + 15) / mvbk::kUnit + 2;
     const size_t d = kHeaderBytes + 16 * fs + 20 * (fs / 31 + 2 * mvbk::kFLevels) + 16 * mvbk::kFLevels;
-    return std::max(std::max(a, b), std::max(c, d));
+    // (a permissive decode keeps the per-tile kernel's arrays after the fused tree)
+    return std::max(std::max(a + d, b), c);
 }
 
 int mvb_workspace_init(void* ws, size_t ws_bytes, mvb_stream_t stream) {
