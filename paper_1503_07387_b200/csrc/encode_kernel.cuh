@@ -100,16 +100,36 @@ __global__ void __launch_bounds__(1024) vbyte_enc_scan(unsigned long long* tile_
 template <bool kDelta>
 __global__ void __launch_bounds__(kEncThreads) vbyte_enc_write(const uint32_t* v, unsigned long long n,
                                                               const unsigned long long* tile_off, uint8_t* out) {
+    // The tile's bytes are assembled in shared memory at the same offset modulo 16
+    // as their place in `out`, then copied out as aligned 16-byte chunks (the
+    // ragged first and last chunk byte by byte): the threads' runs of 16..80
+    // bytes never go to global memory one byte at a time.
+    __shared__ __align__(16) uint8_t s_out[kEncTile * 5 + 32];
     __shared__ unsigned long long s_w[kEncThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned long long i0 = static_cast<unsigned long long>(blockIdx.x) * kEncTile + threadIdx.x * kEncPer;
     uint32_t x[kEncPer];
     unsigned long long bytes = 0;
+    if (i0 + kEncPer <= n && !kDelta && (reinterpret_cast<uintptr_t>(v) & 15u) == 0u) {
+        // (a thread's 16 values are 64 contiguous bytes, 16-byte aligned if v is)
+        const uint4* q = reinterpret_cast<const uint4*>(v + i0);
 #pragma unroll
-    for (int k = 0; k < kEncPer; ++k) {
-        const unsigned long long i = i0 + k;
-        x[k] = i < n ? enc_value<kDelta>(v, i) : 0u;
-        bytes += i < n ? enc_size(x[k]) : 0u;
+        for (int k = 0; k < kEncPer / 4; ++k) {
+            const uint4 t = __ldg(q + k);
+            x[4 * k] = t.x;
+            x[4 * k + 1] = t.y;
+            x[4 * k + 2] = t.z;
+            x[4 * k + 3] = t.w;
+        }
+#pragma unroll
+        for (int k = 0; k < kEncPer; ++k) bytes += enc_size(x[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kEncPer; ++k) {
+            const unsigned long long i = i0 + k;
+            x[k] = i < n ? enc_value<kDelta>(v, i) : 0u;
+            bytes += i < n ? enc_size(x[k]) : 0u;
+        }
     }
     unsigned long long incl = bytes;
 #pragma unroll
@@ -119,11 +139,15 @@ __global__ void __launch_bounds__(kEncThreads) vbyte_enc_write(const uint32_t* v
     }
     if (lane == 31) s_w[wid] = incl;
     __syncthreads();
-    unsigned long long wbase = 0;
+    unsigned long long wbase = 0, total = 0;
 #pragma unroll
-    for (int k = 0; k < kEncThreads / 32; ++k)
+    for (int k = 0; k < kEncThreads / 32; ++k) {
         if (k < wid) wbase += s_w[k];
-    uint8_t* p = out + tile_off[blockIdx.x] + wbase + incl - bytes;
+        total += s_w[k];
+    }
+    uint8_t* const dst = out + tile_off[blockIdx.x];
+    const uint32_t a = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15u);
+    uint8_t* p = s_out + a + static_cast<uint32_t>(wbase + incl - bytes);
 #pragma unroll
     for (int k = 0; k < kEncPer; ++k) {
         if (i0 + k < n) {
@@ -133,6 +157,17 @@ __global__ void __launch_bounds__(kEncThreads) vbyte_enc_write(const uint32_t* v
                 y >>= 7;
             }
             *p++ = static_cast<uint8_t>(y);
+        }
+    }
+    __syncthreads();
+    const uint32_t end = a + static_cast<uint32_t>(total);  // s_out[a, end) <-> (dst - a)[a, end)
+    uint8_t* const base = dst - a;                          // 16-byte aligned
+    for (uint32_t c = threadIdx.x; 16u * c < end; c += kEncThreads) {
+        const uint32_t lo = 16u * c, hi = lo + 16u;
+        if (lo >= a && hi <= end) {
+            *reinterpret_cast<uint4*>(base + lo) = *reinterpret_cast<const uint4*>(s_out + lo);
+        } else {
+            for (uint32_t b = lo > a ? lo : a; b < (hi < end ? hi : end); ++b) base[b] = s_out[b];
         }
     }
 }

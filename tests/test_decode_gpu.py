@@ -472,6 +472,13 @@ def test_device_encoder_matches_reference_encoder(cuda, oracle):
         got = mvb.encode_device(torch.from_numpy(s.view(np.int32)).to(cuda), deltas=True).cpu().numpy()
         gaps = np.diff(np.concatenate([[0], s.astype(np.int64)])).astype(np.uint32)
         np.testing.assert_array_equal(got, oracle.encode_sequence(gaps), err_msg=f"deltas n={n}")
+    # input and output at odd alignments (the encoder's vector loads and aligned chunk stores)
+    v = W.mixed_values(70001, 9)
+    for off in (1, 2, 3):
+        t = torch.zeros(v.size + 8, dtype=torch.int32, device=cuda)
+        t[off:off + v.size] = torch.from_numpy(v.view(np.int32)).to(cuda)
+        got = mvb.encode_device(t[off:off + v.size]).cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.encode_sequence(v), err_msg=f"input offset {off}")
     v = np.sort(W.mixed_values(50000, 1))
     v[31337] = v[31336] - 1 if v[31336] else 5
     v[40000] = 0
