@@ -59,6 +59,9 @@ namespace mvbk {
 #ifndef MVB_F_STATIC0
 #define MVB_F_STATIC0 8  // streams of fewer than this many units per warp: the first round of units without tickets (0: never)
 #endif
+#ifndef MVB_F_SLEEP
+#define MVB_F_SLEEP 32  // ns between two looks at a tree entry not yet published
+#endif
 #ifndef MVB_F_LATE
 #define MVB_F_LATE 0  // 1: a unit's prefix entries are checked (and waited for) after the next unit's publication
 #endif
@@ -890,7 +893,7 @@ __device__ __forceinline__ void fentry_get(const FEntry* e, unsigned tag, unsign
     for (;;) {
         asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(s) : "l"(e) : "memory");
         if ((c & 0xFFFFFFull) == tag && (s & 0xFFFFFFull) == tag) break;
-        __nanosleep(32);
+        __nanosleep(MVB_F_SLEEP);
     }
     cnt = c >> 24;
     sum = static_cast<uint32_t>(s >> 32);
@@ -1050,7 +1053,7 @@ __device__ __forceinline__ void fused_prefix_finish_n(const FusedParams& F, uint
         if (static_cast<uint32_t>(lane) < (vl & 31u)) {
             unsigned long long pc = P.c[l], ps = P.s[l];
             while ((static_cast<uint32_t>(pc) & 0xFFFFFFu) != tag || (static_cast<uint32_t>(ps) & 0xFFFFFFu) != tag) {
-                __nanosleep(32);
+                __nanosleep(MVB_F_SLEEP);
                 const FEntry* e = F.tree[l] + ((vl & ~31u) + static_cast<uint32_t>(lane));
                 asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(pc), "=l"(ps) : "l"(e) : "memory");
             }
