@@ -713,16 +713,20 @@ __device__ __noinline__ bool unit_d3_checked(uint32_t ubuf, uint32_t* op, uint32
 // decode_range_ll's per-slice algorithm over the unit [qs, qe) staged in
 // shared memory at ubuf (byte qs; the 16 bytes before it too), or -- ubuf 0,
 // units at the stream's edges -- read from global memory with range masks.
-template <bool kDelta, bool kSwz>
+// kIn: the unit is staged, lies inside the stream with the 16 bytes before it,
+// and all its integers end before `limit` -- every slice is interior, nothing
+// is masked or clipped, no slice holds integer limit-1 (plain streams' common
+// units: the range logic below was a fifth of c1's instructions).
+template <bool kDelta, bool kSwz, bool kIn = false>
 __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs, long long qe,
                                                 unsigned long long base, uint32_t carry, unsigned long long limit,
                                                 uint32_t* out, uint32_t* stage, uint32_t ubuf, int lane,
                                                 const RangeSink& K, RangeOut& ro, unsigned long long pol) {
     const uint32_t out_w = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(out) >> 2);
     const uint32_t st_base = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-    const int ns = static_cast<int>((qe - qs + kLLSlice - 1) / kLLSlice);
-    int i_lo, i_hi;  // interior slices: i_lo <= i < i_hi
-    {
+    const int ns = kIn ? kUnit / kLLSlice : static_cast<int>((qe - qs + kLLSlice - 1) / kLLSlice);
+    int i_lo = 0, i_hi = ns;  // interior slices: i_lo <= i < i_hi
+    if (!kIn) {
         const long long d = R.lo - qs, e = R.hi - qs;
         const long long lo = d <= 0 ? 0 : (d + kLLSlice - 1) / kLLSlice;
         const long long hi = e <= 0 ? 0 : e / kLLSlice;
@@ -747,10 +751,10 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
 #pragma unroll 1
     for (int i = 0; i < ns; ++i) {
         const uint32_t a = (out_w + static_cast<uint32_t>(run)) & 3u;  // staging offset of the slice
-        const bool inter = i >= i_lo && i < i_hi;                      // warp-uniform
+        const bool inter = kIn || (i >= i_lo && i < i_hi);             // warp-uniform
         const long long q0 = qs + static_cast<long long>(kLLSlice) * i + 32 * lane;
         uint4 x0, x1;
-        if (inter && ubuf) {
+        if (kIn || (inter && ubuf)) {
             const uint32_t sa = ubuf + static_cast<uint32_t>(kLLSlice * i + 32 * lane);
             x0 = lds128(sa);
             x1 = lds128(sa + 16u);
@@ -829,7 +833,7 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
             carry += hin;
             lane_slots_d3<kSwz>(wp3, w, T32 & inr32, st_base + 4u * (a + wexcl), carry);
             carry -= hout;
-            if (run < limit && run + n_w >= limit)
+            if (!kIn && run < limit && run + n_w >= limit)
                 slice_count_end(R, K, q0, T32 & inr32, static_cast<uint32_t>(limit - 1 - run), wexcl, n_own);
         } else if (take2 || takef || takef5) {
             if (take2)
@@ -840,7 +844,7 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
                 lane_slots_fast<kDelta, kSwz>(wp3, w, T32, st_base + 4u * (a + wexcl), carry);
             // the slice holds integer limit-1: record its end (stores past limit are
             // dropped by the copy-out)
-            if (run < limit && run + n_w >= limit)
+            if (!kIn && run < limit && run + n_w >= limit)
                 slice_count_end(R, K, q0, T32 & inr32, static_cast<uint32_t>(limit - 1 - run), wexcl, n_own);
         } else
             carry = ll_slice_gen<kDelta, kSwz>(R, q0, x0, x1, wp2, wp3, T32, inr32, n_w, wexcl, run, limit, K,
@@ -850,13 +854,14 @@ __device__ __forceinline__ void decode_unit_ll(const ByteRange& R, long long qs,
         if (!kSwz) {
             stage_fence();
             __syncwarp();
-            stage_out_bulk(st_base, a, n_w, run, limit, out, lane, pol);
+            if (kIn) stage_out_d3(st_base, a, a + n_w, out + run - a, lane, pol);
+            else stage_out_bulk(st_base, a, n_w, run, limit, out, lane, pol);
             run += n_w;
             continue;
         }
 #endif
         __syncwarp();
-        stage_out<kSwz>(st_base, a, n_w, run, limit, out, lane);
+        stage_out<kSwz>(st_base, a, n_w, run, kIn ? ~0ull : limit, out, lane);
         run += n_w;
         __syncwarp();  // the staging buffer is rewritten by the next slice
     }
@@ -1354,7 +1359,16 @@ __global__ void __launch_bounds__(kSegThreads, kFBlocks) vbyte_fused_decode(cons
                 }
                 const uint32_t carry = kDelta ? csum - straddle + prev0 : 0u;
                 RangeOut ro;
-                if (swz)
+                // (plain streams: the common units -- staged, whole, before the count limit --
+                // through the range-logic-free instantiation)
+                const bool in_unit = !kDelta && up >= u_first && up < u_end && base + c_up < S.count;
+                if (!kDelta && in_unit && swz)
+                    decode_unit_ll<kDelta, true, !kDelta>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                          ro, pol);
+                else if (!kDelta && in_unit)
+                    decode_unit_ll<kDelta, false, !kDelta>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
+                                                           ro, pol);
+                else if (swz)
                     decode_unit_ll<kDelta, true>(R, qs, qe, base, carry, S.count, S.out, stage, ubuf, lane, K,
                                                  ro, pol);
                 else
