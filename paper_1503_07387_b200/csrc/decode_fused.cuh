@@ -59,6 +59,9 @@ namespace mvbk {
 #ifndef MVB_F_STATIC0
 #define MVB_F_STATIC0 8  // streams of fewer than this many units per warp: the first round of units without tickets (0: never)
 #endif
+#ifndef MVB_OUT_PRED
+#define MVB_OUT_PRED 1  // the d3 copy-out as predicated instructions instead of branches (c4 987 -> 932 us)
+#endif
 #ifndef MVB_F_SLEEP
 #define MVB_F_SLEEP 32  // ns between two looks at a tree entry not yet published
 #endif
@@ -382,6 +385,24 @@ __device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t first, u
     const uint32_t i0 = (first + 3u) & ~3u, i1 = end & ~3u;
     // (the copied range lies in the staging buffer; the bulk copy's ends are 16-byte aligned)
     MVB_CHECK(first <= end && end <= static_cast<uint32_t>(kFStage) && (reinterpret_cast<uintptr_t>(ob) & 15u) == 0u);
+#if MVB_OUT_PRED
+    // branch-free: every lane computes its (possibly unused) single integer's
+    // place -- lanes 0..3 the head quad's [first, i0), lanes 4..7 the tail quad's
+    // [i1, end) -- and the copies are predicated instructions
+    const uint32_t i = lane < 4 ? (first & ~3u) + static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+    const uint32_t p1 = (lane < 8 && i < end && (lane < 4 ? (i >= first && i < i0) : i >= i0)) ? 1u : 0u;
+    const uint32_t p2 = (lane == 0 && i1 > i0) ? 1u : 0u;
+    const uint32_t p3 = lane == 0 ? 1u : 0u;
+    asm volatile(
+        "{\n\t.reg .pred q1, q2, q3;\n\t.reg .b32 v;\n\t"
+        "setp.ne.b32 q1, %0, 0;\n\tsetp.ne.b32 q2, %1, 0;\n\tsetp.ne.b32 q3, %2, 0;\n\t"
+        "@q1 ld.shared.u32 v, [%3];\n\t@q1 st.global.cs.u32 [%4], v;\n\t"
+        "@q2 cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%5], [%6], %7, %8;\n\t"
+        "@q3 cp.async.bulk.commit_group;\n\t}"
+        ::"r"(p1), "r"(p2), "r"(p3), "r"(st_base + 4u * i), "l"(ob + i), "l"(ob + i0), "r"(st_base + 4u * i0),
+          "r"(4u * (i1 - i0)), "l"(pol)
+        : "memory");
+#else
     if (lane < 8) {
         const uint32_t i = lane < 4 ? (first & ~3u) + static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
         if (lane < 4 ? (i >= first && i < i0 && i < end) : (i < end && i >= i0)) {
@@ -397,6 +418,7 @@ __device__ __forceinline__ void stage_out_d3(uint32_t st_base, uint32_t first, u
                          : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+#endif
 }
 
 // op (in/out): the slice's first output, out + its index.

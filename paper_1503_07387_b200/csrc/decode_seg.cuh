@@ -1302,8 +1302,16 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
 //              buffer); __syncwarp(); st.shared ...
 // and stage_wait_all() before the warp's last instruction.
 __device__ __forceinline__ void stage_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+#ifndef MVB_WAIT_PRED
+#define MVB_WAIT_PRED 1  // stage_wait_read as a predicated instruction instead of a branch (c4 931 -> 917 us)
+#endif
 __device__ __forceinline__ void stage_wait_read(int lane) {
+#if MVB_WAIT_PRED
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %0, 0;\n\t@q cp.async.bulk.wait_group.read 0;\n\t}" ::"r"(lane)
+                 : "memory");
+#else
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void stage_wait_all(int lane) {
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
