@@ -1328,21 +1328,20 @@ __device__ __forceinline__ void stage_out_bulk(uint32_t st_base, uint32_t a, uin
 #if MVB_CHECKS
     assert(a < 4u && end <= a + n && g0 + end <= limit && g0 + a == run);
 #endif
-    if (lane < 8) {
-        const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
-        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {
-            uint32_t v;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(st_base + 4u * i) : "memory");
-            __stcs(ob + i, v);
-        }
-    }
-    if (lane == 0) {
-        if (i1 > i0)
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(ob + i0),
-                         "r"(st_base + 4u * i0), "r"(4u * (i1 - i0)), "l"(pol)
-                         : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
+    // (predicated instructions instead of single-lane branches, as stage_out_d3)
+    const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
+    const uint32_t p1 = (lane < 8 && (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0))) ? 1u : 0u;
+    const uint32_t p2 = (lane == 0 && i1 > i0) ? 1u : 0u;
+    const uint32_t p3 = lane == 0 ? 1u : 0u;
+    asm volatile(
+        "{\n\t.reg .pred q1, q2, q3;\n\t.reg .b32 v;\n\t"
+        "setp.ne.b32 q1, %0, 0;\n\tsetp.ne.b32 q2, %1, 0;\n\tsetp.ne.b32 q3, %2, 0;\n\t"
+        "@q1 ld.shared.u32 v, [%3];\n\t@q1 st.global.cs.u32 [%4], v;\n\t"
+        "@q2 cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%5], [%6], %7, %8;\n\t"
+        "@q3 cp.async.bulk.commit_group;\n\t}"
+        ::"r"(p1), "r"(p2), "r"(p3), "r"(st_base + 4u * i), "l"(ob + i), "l"(ob + i0), "r"(st_base + 4u * i0),
+          "r"(4u * (i1 - i0)), "l"(pol)
+        : "memory");
 }
 
 
