@@ -1256,13 +1256,15 @@ __device__ __forceinline__ void stage_out(uint32_t st_base, uint32_t a, uint32_t
     // every store of this copy-out lies in out[run, min(run + n, limit))
     assert(a < 4u && end <= a + n && g0 + end <= limit && g0 + a == run);
 #endif
-    if (lane < 8) {
+    {
+        // (predicated instructions instead of a branch for lanes 0..7, as stage_out_d3)
         const uint32_t i = lane < 4 ? static_cast<uint32_t>(lane) : i1 + static_cast<uint32_t>(lane - 4);
-        if (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0)) {
-            uint32_t v;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(stg_addr<kSwz>(st_base + 4u * i)) : "memory");
-            __stcs(ob + i, v);
-        }
+        const uint32_t p1 = (lane < 8 && (lane < 4 ? (i >= a && i < end && a != 0) : (i < end && i1 >= i0))) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred q1;\n\t.reg .b32 v;\n\tsetp.ne.b32 q1, %0, 0;\n\t"
+            "@q1 ld.shared.u32 v, [%1];\n\t@q1 st.global.cs.u32 [%2], v;\n\t}"
+            ::"r"(p1), "r"(stg_addr<kSwz>(st_base + 4u * i)), "l"(ob + i)
+            : "memory");
     }
     // whole quads: lane l copies quads q = i0/4 + l + 32m.  Swizzled, quad q
     // sits at q ^ ((q >> 3) & 7), and (q >> 3) & 7 only flips bit 2 from one m
